@@ -1,0 +1,223 @@
+"""Generate golden vectors by running the REFERENCE implementation.
+
+Run in the build container only (it imports /root/reference, which does not
+exist on the GPU box):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Outputs (committed):
+  tests/golden/golden.npz     -- inputs (small) and reference outputs
+  tests/golden/golden.json    -- metadata: versions, per-config instance hashes
+  tests/golden/gr17_base.json -- the reference's parse of pkg/data/gr17.tsp
+
+Reference functions exercised (paths relative to pkg/src/vrp_rpd/):
+  instance.parse_tsplib / build_instance   instance.py:200-401
+  schedule.exact_makespan                  schedule.py:265-316
+  schedule.evaluate                        schedule.py:188-257
+  schedule.two_pass_estimate               schedule.py:345-393
+  brkga.decode / encode                    brkga.py:92-222
+  brkga.evolve (Generator(Philox) injected) brkga.py:231-252
+"""
+from __future__ import annotations
+
+import json
+import platform
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+REPO = HERE.parent.parent
+REF_SRC = Path("/root/reference/pkg/src")
+REF_DATA = Path("/root/reference/pkg/data")
+sys.path.insert(0, str(REF_SRC))
+sys.path.insert(0, str(REPO))
+sys.path.insert(0, str(HERE))
+
+import vrp_rpd  # noqa: E402  (the reference)
+from vrp_rpd import brkga as R_brkga  # noqa: E402
+from vrp_rpd import instance as R_inst  # noqa: E402
+from vrp_rpd import schedule as R_sched  # noqa: E402
+
+import inputs as I  # noqa: E402
+from paper_2602_23685_b200 import configs as C  # noqa: E402
+from paper_2602_23685_b200 import instance as mine  # noqa: E402
+
+STATUS = {None: 0, "CapacityViolation": 1, "Deadlock": 2, "MalformedSolution": 3}
+CFG_ID = {"gr17": 1, "eil51": 2, "kroA100": 3, "a280": 4, "dsj1000": 5}
+# (decode chromosomes, random candidates, block candidates)
+COUNTS = {"gr17": (256, 256, 64), "eil51": (96, 128, 32), "kroA100": (48, 64, 16),
+          "a280": (16, 32, 8), "dsj1000": (8, 16, 4)}
+
+
+def ref_instance(key):
+    spec = C.CONFIGS[key]
+    if spec.edge_type == "EXPLICIT":
+        raw = R_inst.load_tsplib_file(REF_DATA / "gr17.tsp")
+    else:
+        raw = R_inst.parse_tsplib(C.synthetic_tsplib(spec))
+    return R_inst.build_instance(raw, R_inst.VariantSpec(spec.variant, C.VARIANT_SEED, 0))
+
+
+def to_solution(ops_row, lens_row):
+    return R_sched.Solution.from_lists(
+        [[(c, R_sched.OpKind(k)) for c, k in t] for t in I.arrays_to_lists(ops_row, lens_row)])
+
+
+def score(inst, ops, lens):
+    """Reference exact_makespan / evaluate / two_pass on each candidate."""
+    N = ops.shape[0]
+    out = {k: np.zeros(N) for k in ("z_exact", "z_eval", "z_two")}
+    out.update({k: np.zeros(N, np.int32) for k in ("st_exact", "st_eval", "st_two")})
+    out["returns"] = np.zeros((N, inst.m))
+    for i in range(N):
+        sol = to_solution(ops[i], lens[i])
+        for fn, tag in ((R_sched.exact_makespan, "exact"), (None, "eval"),
+                        (R_sched.two_pass_estimate, "two")):
+            try:
+                if tag == "eval":
+                    sch = R_sched.evaluate(inst, sol)
+                    z = sch.makespan
+                    out["returns"][i] = sch.returns
+                else:
+                    z = fn(inst, sol)
+                st = 0
+            except R_sched.ScheduleError as exc:
+                z, st = 0.0, STATUS[type(exc).__name__]
+            out[f"z_{tag}"][i] = z
+            out[f"st_{tag}"][i] = st
+    return out
+
+
+def main():
+    t0 = time.time()
+    blob: dict = {}
+    meta = {"python": platform.python_version(), "numpy": np.__version__,
+            "reference": str(REF_SRC), "configs": {}}
+
+    for key, spec in C.CONFIGS.items():
+        cid = CFG_ID[key]
+        n_dec, n_rand, n_blk = COUNTS[key]
+        inst = ref_instance(key)
+        d = np.array(inst.d, dtype=np.float64)
+        p = np.array(inst.p, dtype=np.float64)
+        n, m, k = inst.n, inst.m, inst.k
+        if key == "gr17":
+            inst.save(HERE / "gr17_base.json")
+        # pin our own instance builder against the reference's
+        ours = C.config_instance(key)
+        od, op = ours.arrays()
+        assert np.array_equal(od, d) and np.array_equal(op, p), key
+        assert (ours.n, ours.m, ours.k) == (n, m, k), key
+        meta["configs"][key] = {"n": n, "m": m, "k": k, "label": inst.label,
+                                "d_sha": I.sha(d), "p_sha": I.sha(p),
+                                "integral": bool(np.all(d == np.round(d)) and np.all(p == np.round(p)))}
+        pre = f"{key}/"
+        blob[pre + "p"] = p
+        if n <= 100:
+            blob[pre + "d"] = d
+
+        # ---- decode: uniform chromosomes, encoded (tie-heavy) ones, strict mode
+        genes = I.chromosomes(n, n_dec, (136, cid))
+        params = R_brkga.BrkgaParams(population=max(20, n_dec))
+        strict = R_brkga.BrkgaParams(population=max(20, n_dec), wait_relaxation=False)
+        dec_ops = np.zeros((n_dec, 2 * n), np.int32)
+        dec_lens = np.zeros((n_dec, m), np.int32)
+        recs = {k2: [] for k2 in ("fitness", "makespan", "scheduled", "visits")}
+        enc = []
+        for i in range(n_dec):
+            r = R_brkga.decode(genes[i], inst, params)
+            o, l = I.lists_to_arrays([[(c, kd.value) for c, kd in t] for t in r.solution.tours], n)
+            dec_ops[i], dec_lens[i] = o, l
+            recs["fitness"].append(r.fitness)
+            recs["makespan"].append(r.makespan)
+            recs["scheduled"].append(r.scheduled_count)
+            recs["visits"].append(r.op_visits)
+            if i < max(2, n_dec // 8):
+                enc.append(R_brkga.encode(inst, r.solution))
+        blob[pre + "dec_genes_sha"] = np.frombuffer(I.sha(genes).encode(), np.uint8)
+        blob[pre + "dec_ops"] = dec_ops
+        blob[pre + "dec_lens"] = dec_lens
+        for k2, v in recs.items():
+            blob[pre + "dec_" + k2] = np.array(v)
+        # encoded chromosomes (many exactly-equal keys) + strict-mode decodes
+        enc = np.array(enc)
+        blob[pre + "enc_genes"] = enc
+        for tag, prm, src in (("enc", params, enc), ("strict", strict, genes[: len(enc)])):
+            o_all = np.zeros((len(src), 2 * n), np.int32)
+            l_all = np.zeros((len(src), m), np.int32)
+            fit, mk, sc, vi = [], [], [], []
+            for i in range(len(src)):
+                r = R_brkga.decode(src[i], inst, prm)
+                o_all[i], l_all[i] = I.lists_to_arrays(
+                    [[(c, kd.value) for c, kd in t] for t in r.solution.tours], n)
+                fit.append(r.fitness); mk.append(r.makespan)
+                sc.append(r.scheduled_count); vi.append(r.op_visits)
+            blob[pre + f"{tag}_ops"] = o_all
+            blob[pre + f"{tag}_lens"] = l_all
+            blob[pre + f"{tag}_fitness"] = np.array(fit)
+            blob[pre + f"{tag}_makespan"] = np.array(mk)
+            blob[pre + f"{tag}_scheduled"] = np.array(sc)
+            blob[pre + f"{tag}_visits"] = np.array(vi)
+
+        # ---- makespan family on decoded / random / block / perturbed candidates
+        rnd_ops, rnd_lens = I.random_candidates(n, m, n_rand, (136, cid, 1))
+        blk_ops, blk_lens = I.block_candidates(n, m, k, n_blk, (136, cid, 2))
+        swp_ops = I.swap_perturb(dec_ops, dec_lens, (136, cid, 3))
+        # malformed: duplicate one op in a few decoded candidates
+        mal_ops = dec_ops[: min(4, n_dec)].copy()
+        if n > 1:
+            mal_ops[:, 1] = mal_ops[:, 0]
+        sets = {"dec": (dec_ops, dec_lens), "rnd": (rnd_ops, rnd_lens),
+                "blk": (blk_ops, blk_lens), "swp": (swp_ops, dec_lens),
+                "mal": (mal_ops, dec_lens[: len(mal_ops)])}
+        for tag, (o, l) in sets.items():
+            if tag != "dec":
+                blob[pre + f"{tag}_ops"] = o
+                blob[pre + f"{tag}_lens"] = l
+            res = score(inst, o, l)
+            for k2, v in res.items():
+                blob[pre + f"{tag}_{k2}"] = v
+        print(f"{key}: n={n} m={m} k={k} done at {time.time() - t0:.1f}s", flush=True)
+
+    # ---- evolve with an injected Generator(Philox)
+    ev = []
+    for j, (N, G, frac_e, frac_m, bias, tie) in enumerate([
+            (20, 8, 0.15, 0.15, 0.7, False), (60, 64, 0.15, 0.15, 0.7, True),
+            (200, 200, 0.15, 0.15, 0.7, True), (257, 120, 0.2, 0.1, 0.6, False),
+            (10, 6, 0.15, 0.15, 1.0, False), (1000, 32, 0.15, 0.15, 0.7, True)]):
+        g = I.philox(7, j)
+        pop = g.random((N, G))
+        fit = g.random(N)
+        if tie:
+            fit = np.round(fit * 7.0)
+        rng = I.philox(11, j)
+        prm = R_brkga.BrkgaParams(population=N, elite_fraction=frac_e,
+                                  mutant_fraction=frac_m, elite_bias=bias)
+        out = R_brkga.evolve(pop, fit, prm, rng)
+        st = rng.bit_generator.state
+        blob[f"evolve/{j}/out"] = out
+        ev.append({"N": N, "G": G, "elite": frac_e, "mutant": frac_m, "bias": bias,
+                   "tie": tie, "pop_key": [7, j], "rng_key": [11, j],
+                   "final_counter": [int(x) for x in st["state"]["counter"]],
+                   "final_buffer_pos": int(st["buffer_pos"]),
+                   "final_has_uint32": int(st["has_uint32"]),
+                   "final_uinteger": int(st["uinteger"])})
+    meta["evolve"] = ev
+
+    # ---- hint vehicle edge cases (brkga.py:82-89)
+    genes = np.array([0.0, 1 / 3, 2 / 3, 1 / 6, 0.5, np.nextafter(1.0, 0), 0.999999999,
+                      np.nextafter(1 / 3, 0), np.nextafter(2 / 3, 0), 0.2, 0.4, 0.6, 0.8])
+    hv = np.array([[R_brkga._hint_vehicle(mm, float(x)) for x in genes] for mm in (1, 2, 3, 5, 6, 7)])
+    blob["hint/genes"] = genes
+    blob["hint/out"] = hv
+
+    np.savez_compressed(HERE / "golden.npz", **blob)
+    (HERE / "golden.json").write_text(json.dumps(meta, indent=1))
+    print(f"wrote golden in {time.time() - t0:.1f}s")
+
+
+if __name__ == "__main__":
+    main()
