@@ -1,0 +1,329 @@
+"""Headline benchmark: candidate makespan evaluations/s at n = 999 (dsj1000-derived, 1R20).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+A step = one launch of K1 (exact_makespan, csrc/makespan.cu) over this rank's
+whole batch of N_CAND candidates, which are decoded (K3, untimed setup) from
+seeded uniform random chromosomes, so every candidate is feasible and unique.
+The batch (2^20 x 1998 int16 ops = 4.2 GB) is far larger than the 126 MB L2, so
+no flush is needed between steps.  Multi-GPU: one process per GPU (torchrun),
+each rank scores its own candidates (weak scaling, no data-path collective);
+time = max over ranks of the CUDA-event time.
+
+``--impl reference`` times the reference algorithm on the host CPU: the C
+restatement in oracle/ (the reference itself is pure Python and not built),
+with every host thread, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+sys.path.insert(0, str(REPO / "tests" / "golden"))
+
+CONFIG = "dsj1000"
+METRIC = "candidate makespan evals/sec at n=1000"
+UNIT = "evals/s"
+
+
+def algorithmic_bytes_per_eval(n: int, m: int) -> int:
+    """ops 4*2n + lens 4m + d gathers 8*(2n+m) + p gathers 8n + 12 B out."""
+    return 4 * 2 * n + 4 * m + 8 * (2 * n + m) + 8 * n + 12
+
+
+def measured_peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        doc = json.loads(p.read_text())
+        return float(doc["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+               0x2: "applications_clocks_setting", 0x10: "sync_boost", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period: float = 0.02):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_reference_rate(inst, ops, lens, threads: int, min_seconds: float):
+    """Oracle (C restatement of schedule.exact_makespan) on host threads."""
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    done = 0
+    while True:
+        O.makespan_batch(inst, ops, lens, mode="exact", threads=threads)
+        done += ops.shape[0]
+        el = time.perf_counter() - t0
+        if el >= min_seconds:
+            return done / el, done, el
+
+
+def make_candidates(inst, count: int, seed: int, device, chunk: int = 1 << 16):
+    """Decode `count` seeded random chromosomes on the GPU (K3) -> int16 ops."""
+    import torch
+    from paper_2602_23685_b200 import device as D
+    n, m = inst.n, inst.m
+    ops = torch.empty((count, 2 * n), dtype=torch.int16, device=device)
+    lens = torch.empty((count, m), dtype=torch.int32, device=device)
+    z = torch.empty(count, dtype=torch.float64, device=device)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    for s in range(0, count, chunk):
+        e = min(count, s + chunk)
+        genes = torch.rand((e - s, 4 * n), dtype=torch.float64, device=device, generator=gen)
+        out = {"ops": ops[s:e], "lens": lens[s:e]}
+        r = D.decode_batch(inst, genes, out=out)
+        z[s:e] = r["makespan"]
+        del genes
+    return ops, lens, z
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import inputs as I
+    from oracle import oracle as O
+    from paper_2602_23685_b200.configs import config_instance
+    inst = config_instance(CONFIG)
+    threads = O.default_threads()
+    genes = I.chromosomes(inst.n, 2048, (136, 5000))
+    dec = O.decode_batch(inst, genes, threads=threads)
+    ops, lens = dec["ops"], dec["lens"]
+    for _ in range(args.warmup):
+        O.makespan_batch(inst, ops[:256], lens[:256], mode="exact", threads=threads)
+    rates = []
+    for _ in range(args.steps):
+        r, _, _ = cpu_reference_rate(inst, ops, lens, threads, min_seconds=0.5)
+        rates.append(r)
+    value = float(statistics.median(rates))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * ops.shape[0] / value, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{CONFIG}-derived 1R20 (n=999, m=6, k=4): exact_makespan "
+                                   f"of {ops.shape[0]} decoded candidates per step, host CPU",
+                       "n": inst.n, "m": inst.m, "k": inst.k},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{ops.shape[0]} oracle-decoded dsj1000 candidates, "
+                                       f">=0.5 s per step, {threads} threads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2602_23685_b200 import device as D
+    from paper_2602_23685_b200.configs import config_instance
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    inst = config_instance(CONFIG)
+    n, m = inst.n, inst.m
+    n_cand = args.candidates
+
+    t_setup = time.perf_counter()
+    ops, lens, z_dec = make_candidates(inst, n_cand, seed=1000 + rank, device=dev)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+
+    stream = torch.cuda.current_stream()
+    out = {}
+    D.makespan_batch(inst, ops, lens, mode=0, out=out)
+    torch.cuda.synchronize()
+    # sanity: K1 must reproduce the decoder's makespans
+    if not (bool((out["status"] == 0).all()) and torch.equal(out["z"], z_dec)):
+        raise SystemExit("bench: K1 disagrees with the decoder's makespans")
+
+    for _ in range(args.warmup):
+        D.makespan_batch(inst, ops, lens, mode=0, out=out)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            D.makespan_batch(inst, ops, lens, mode=0, out=out)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    total_units = n_cand * world
+    value = total_units * args.steps / (ms / 1e3)
+
+    # ---- end to end through the public API: pinned host ops -> GPU -> host z/status
+    e2e = None
+    if not args.no_e2e:
+        ne = min(n_cand, args.e2e_candidates)
+        h_ops = torch.empty((ne, 2 * n), dtype=torch.int16, pin_memory=True)
+        h_lens = torch.empty((ne, m), dtype=torch.int32, pin_memory=True)
+        h_ops.copy_(ops[:ne])
+        h_lens.copy_(lens[:ne])
+        from paper_2602_23685_b200.schedule import score_host_batch
+        res = score_host_batch(inst, h_ops, h_lens)  # warm
+        torch.cuda.synchronize()
+        steps_e = max(3, args.steps // 4)
+        for _ in range(2):
+            score_host_batch(inst, h_ops, h_lens)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps_e):
+            res = score_host_batch(inst, h_ops, h_lens)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        assert np.array_equal(res[0], z_dec[:ne].cpu().numpy())
+        e2e = {"value": ne * world * steps_e / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(ne * (2 * n * 2 + m * 4)),
+               "d2h_bytes_per_step": int(ne * (8 + 4)),
+               "candidates_per_step": ne, "steps": steps_e,
+               "path": "schedule.score_host_batch: pinned int16 ops, chunked H2D/K1/D2H on 2 streams"}
+
+    line = None
+    if rank == 0:
+        peak, peak_kind = measured_peaks()
+        per_eval = algorithmic_bytes_per_eval(n, m)
+        achieved = per_eval * n_cand / (ms_per_step / 1e3) / 1e9  # per GPU, dominant kernel
+        traffic = None
+        tp = REPO / "profiles" / "k1_traffic.json"
+        if tp.exists():
+            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "peak_kind": peak_kind, "bytes_per_eval": per_eval,
+                "note": "algorithmic bytes per SURVEY §8(d) (32n+12m+12); only the op stream "
+                        "is compulsory HBM traffic, d/p gathers are L2-resident"}
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            import inputs as I
+            from oracle import oracle as O
+            threads = O.default_threads()
+            cnt = 2048
+            h = ops[:cnt].to(torch.int32).cpu().numpy()
+            hl = lens[:cnt].cpu().numpy()
+            rate, done, el = cpu_reference_rate(inst, h, hl, threads, min_seconds=args.cpu_seconds)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                   "sample": f"{done} exact_makespan evals ({cnt} distinct decoded dsj1000 "
+                             f"candidates, repeated) in {el:.1f} s on {threads} threads"}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"{CONFIG}-derived 1R20 (n=999, m=6, k=4): exact_makespan "
+                                       f"(K1) of {n_cand} GPU-decoded random-chromosome candidates "
+                                       f"per GPU per step",
+                           "n": n, "m": m, "k": inst.k, "candidates_per_gpu": n_cand,
+                           "op_format": "int16", "l2": "inputs larger than L2 "
+                           f"({n_cand * 2 * n * 2 / 1e9:.1f} GB ops per GPU), no flush",
+                           "parallelism": f"candidate sharding x{world}"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": args.steps, "clocks": clk.summary(),
+                "setup_s": round(setup_s, 2)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--candidates", type=int, default=1 << 20)
+    ap.add_argument("--e2e-candidates", type=int, default=1 << 18)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,96 @@
+/*
+ * vrp_rpd.h -- C-ABI of the B200-native VRP-RPD candidate-scoring library
+ * (libvrprpd.so, built from paper_2602_23685_b200/csrc/ for sm_100a).
+ *
+ * The reference (arxiv 2602.23685, /root/reference/pkg/src/vrp_rpd/) is pure
+ * Python with no FFI of its own; these entry points are what its hot-path
+ * functions would bind (ctypes stub in INTEGRATION.md).  Each export names the
+ * reference function it replaces.
+ *
+ * Conventions
+ *  - Every call returns an int error code: 0 = OK, VRP_EINVAL, VRP_ECUDA,
+ *    VRP_EUNSUPPORTED.  vrp_last_error() gives a message.  No C++ exception
+ *    crosses the ABI.
+ *  - Per-candidate outcomes are status codes, replacing the reference's
+ *    exceptions: VRP_OK, VRP_CAPACITY (CapacityViolation), VRP_DEADLOCK
+ *    (Deadlock), VRP_MALFORMED (MalformedSolution)  (schedule.py:32-45).
+ *  - Batch buffers (ops, lens, genes, outputs) are DEVICE pointers owned by the
+ *    caller; `stream` is a cudaStream_t (NULL = legacy default stream).  Calls
+ *    are asynchronous on that stream.
+ *  - Ops: op code = 2*(customer-1) + kind, kind 0 = dropoff, 1 = pickup
+ *    (brkga.py:73-75 op_index).  One candidate = its m routes concatenated
+ *    vehicle-major; row i starts at ops + i*op_stride elements; lens[i*m + v]
+ *    is route v's length.  op_bytes selects int16 (2) or int32 (4) codes.
+ *  - Times are fp64 and follow the reference's operation order, so results
+ *    are bit-identical to the reference for any input, integer or not.
+ */
+#ifndef VRP_RPD_H
+#define VRP_RPD_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VRP_EINVAL 1
+#define VRP_ECUDA 2
+#define VRP_EUNSUPPORTED 3
+
+#define VRP_OK 0
+#define VRP_CAPACITY 1
+#define VRP_DEADLOCK 2
+#define VRP_MALFORMED 3
+
+/* makespan modes */
+#define VRP_MODE_EXACT 0    /* schedule.exact_makespan  (schedule.py:265-316) */
+#define VRP_MODE_EVALUATE 1 /* schedule.evaluate        (schedule.py:188-257), validating */
+#define VRP_MODE_TWO_PASS 2 /* schedule.two_pass_estimate (schedule.py:345-393) */
+
+typedef struct vrp_instance *vrp_instance_t;
+
+/* Library / device info.  Returns the compiled arch (e.g. 1000 for sm_100a). */
+int vrp_version(int32_t *abi_version, int32_t *compiled_arch);
+const char *vrp_last_error(void);
+
+/* Upload an instance (instance.py:82-156 Instance): host d[(n+1)*(n+1)], p[n+1].
+ * The handle owns the device copies; d is also kept as int32 when every entry
+ * is an integer in [0, 2^31) (all TSPLIB distance types), which halves the
+ * L2 footprint of the gathers.  Requires 1 <= m <= 32, 1 <= n <= 16383. */
+int vrp_instance_create(int32_t n, int32_t m, int32_t k, const double *d_host,
+                        const double *p_host, vrp_instance_t *out);
+int vrp_instance_destroy(vrp_instance_t h);
+int vrp_instance_info(vrp_instance_t h, int32_t *n, int32_t *m, int32_t *k, int32_t *integral);
+
+/* K1/K2: score N candidates.  mode = VRP_MODE_*.
+ * Replaces schedule.exact_makespan / evaluate / two_pass_estimate.
+ *   z[N]            makespan (0 where status != OK)
+ *   status[N]       VRP_OK / CAPACITY / DEADLOCK / MALFORMED
+ *   returns[N*m]    per-vehicle depot return (nullable)      (Schedule.returns)
+ *   bottleneck[N]   first argmax of returns (nullable)       (Schedule.bottleneck, schedule.py:105-110) */
+int vrp_makespan_batch(vrp_instance_t h, const void *ops, int32_t op_bytes, int64_t op_stride,
+                       const int32_t *lens, int64_t N, int32_t mode, double *z, int32_t *status,
+                       double *returns, int32_t *bottleneck, void *stream);
+
+/* Full event records for evaluate (schedule.py:188-257): per op (same layout as
+ * ops) the arrival and execution time, per vehicle the minimal initial load
+ * (route_initial_load, schedule.py:159-185).  Validating (MODE_EVALUATE). */
+int vrp_evaluate_records(vrp_instance_t h, const int32_t *ops, int64_t op_stride,
+                         const int32_t *lens, int64_t N, double *z, int32_t *status,
+                         double *returns, double *arrival, double *time, int32_t *q0,
+                         void *stream);
+
+/* K3: BRKGA decode (brkga.py:92-207) of N chromosomes genes[N][gene_stride]
+ * (4n fp64: priorities then hints).  relax = wait_relaxation, penalty =
+ * infeasibility_penalty.  Outputs: fitness/makespan[N], scheduled[N] (ops
+ * placed), visits[N] (op_visits), and the decoded solution as ops_out (op_bytes
+ * 2|4, row stride out_stride, vehicle-major, unscheduled tail = -1) + lens_out[N*m].
+ * ops_out/lens_out may be NULL when only fitness is needed. */
+int vrp_decode_batch(vrp_instance_t h, const double *genes, int64_t gene_stride, int64_t N,
+                     int32_t relax, double penalty, double *fitness, double *makespan,
+                     int32_t *scheduled, int64_t *visits, void *ops_out, int32_t op_bytes,
+                     int64_t out_stride, int32_t *lens_out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

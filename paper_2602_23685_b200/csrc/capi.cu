@@ -1,0 +1,152 @@
+// capi.cu -- the extern "C" boundary declared in include/vrp_rpd.h.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "../../include/vrp_rpd.h"
+#include "kernels.h"
+
+struct vrp_instance {
+    DevInstance dev;
+    double *d = nullptr;
+    int32_t *d32 = nullptr;
+    double *p = nullptr;
+    int device = 0;
+    int sm_count = 148;
+};
+
+namespace {
+thread_local char g_err[512] = "";
+
+int fail(int code, const char *fmt, const char *arg = "") {
+    snprintf(g_err, sizeof(g_err), fmt, arg);
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *where) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+    return VRP_ECUDA;
+}
+
+int launch_result(int rc, const char *what) {
+    if (rc == 0) return 0;
+    cudaError_t e = cudaGetLastError();
+    if (rc == -2) return fail(VRP_EUNSUPPORTED, "%s: shared-memory footprint exceeds the SM", what);
+    snprintf(g_err, sizeof(g_err), "%s launch failed: %s", what, cudaGetErrorString(e));
+    return VRP_ECUDA;
+}
+}  // namespace
+
+extern "C" {
+
+int vrp_version(int32_t *abi_version, int32_t *compiled_arch) {
+    if (abi_version) *abi_version = 1;
+    if (compiled_arch) *compiled_arch = 1000;
+    return 0;
+}
+
+const char *vrp_last_error(void) { return g_err; }
+
+int vrp_instance_create(int32_t n, int32_t m, int32_t k, const double *d_host, const double *p_host,
+                        vrp_instance_t *out) {
+    if (!out || !d_host || !p_host) return fail(VRP_EINVAL, "null argument%s");
+    if (n < 1 || n > 16383) return fail(VRP_EUNSUPPORTED, "n must lie in [1, 16383]%s");
+    if (m < 1 || m > 32) return fail(VRP_EUNSUPPORTED, "m must lie in [1, 32] (lanes = vehicles)%s");
+    if (k < 1) return fail(VRP_EINVAL, "k must be >= 1%s");
+    const size_t cells = (size_t)(n + 1) * (size_t)(n + 1);
+    bool integral = true;
+    for (size_t i = 0; i < cells && integral; ++i) {
+        double x = d_host[i];
+        if (!(x >= 0.0 && x < 2147483648.0 && x == std::floor(x))) integral = false;
+        if (std::signbit(x)) integral = false;  // keep -0.0 bit-exact in the fp64 table
+    }
+    vrp_instance *h = new (std::nothrow) vrp_instance();
+    if (!h) return fail(VRP_EINVAL, "out of host memory%s");
+    cudaError_t e = cudaGetDevice(&h->device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device);
+    if (e == cudaSuccess) e = cudaMalloc(&h->d, cells * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&h->p, (size_t)(n + 1) * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpy(h->d, d_host, cells * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->p, p_host, (size_t)(n + 1) * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && integral) {
+        int32_t *tmp = new (std::nothrow) int32_t[cells];
+        if (!tmp) { vrp_instance_destroy(h); return fail(VRP_EINVAL, "out of host memory%s"); }
+        for (size_t i = 0; i < cells; ++i) tmp[i] = (int32_t)d_host[i];
+        e = cudaMalloc(&h->d32, cells * sizeof(int32_t));
+        if (e == cudaSuccess) e = cudaMemcpy(h->d32, tmp, cells * sizeof(int32_t), cudaMemcpyHostToDevice);
+        delete[] tmp;
+    }
+    if (e != cudaSuccess) {
+        vrp_instance_destroy(h);
+        return cuda_fail(e, "vrp_instance_create");
+    }
+    h->dev.n = n; h->dev.m = m; h->dev.k = k; h->dev.W = n + 1;
+    h->dev.d = h->d; h->dev.d32 = h->d32; h->dev.p = h->p;
+    h->dev.integral = integral ? 1 : 0;
+    *out = h;
+    return 0;
+}
+
+int vrp_instance_destroy(vrp_instance_t h) {
+    if (!h) return 0;
+    if (h->d) cudaFree(h->d);
+    if (h->d32) cudaFree(h->d32);
+    if (h->p) cudaFree(h->p);
+    delete h;
+    return 0;
+}
+
+int vrp_instance_info(vrp_instance_t h, int32_t *n, int32_t *m, int32_t *k, int32_t *integral) {
+    if (!h) return fail(VRP_EINVAL, "null instance%s");
+    if (n) *n = h->dev.n;
+    if (m) *m = h->dev.m;
+    if (k) *k = h->dev.k;
+    if (integral) *integral = h->dev.integral;
+    return 0;
+}
+
+int vrp_makespan_batch(vrp_instance_t h, const void *ops, int32_t op_bytes, int64_t op_stride,
+                       const int32_t *lens, int64_t N, int32_t mode, double *z, int32_t *status,
+                       double *returns, int32_t *bottleneck, void *stream) {
+    if (!h) return fail(VRP_EINVAL, "null instance%s");
+    if (N < 0 || (N > 0 && (!ops || !lens || !z || !status)))
+        return fail(VRP_EINVAL, "vrp_makespan_batch: null buffer%s");
+    if (op_bytes != 2 && op_bytes != 4) return fail(VRP_EINVAL, "op_bytes must be 2 or 4%s");
+    if (mode < 0 || mode > 2) return fail(VRP_EINVAL, "unknown mode%s");
+    if (N == 0) return 0;
+    int rc = launch_makespan(h->dev, ops, op_bytes, op_stride, lens, N, mode, false, z, status,
+                             returns, bottleneck, nullptr, nullptr, nullptr,
+                             static_cast<cudaStream_t>(stream), h->sm_count);
+    return launch_result(rc, "vrp_makespan_batch");
+}
+
+int vrp_evaluate_records(vrp_instance_t h, const int32_t *ops, int64_t op_stride, const int32_t *lens,
+                         int64_t N, double *z, int32_t *status, double *returns, double *arrival,
+                         double *time, int32_t *q0, void *stream) {
+    if (!h) return fail(VRP_EINVAL, "null instance%s");
+    if (N < 0 || (N > 0 && (!ops || !lens || !z || !status || !arrival || !time)))
+        return fail(VRP_EINVAL, "vrp_evaluate_records: null buffer%s");
+    if (N == 0) return 0;
+    int rc = launch_makespan(h->dev, ops, 4, op_stride, lens, N, 1, true, z, status, returns,
+                             nullptr, arrival, time, q0, static_cast<cudaStream_t>(stream), h->sm_count);
+    return launch_result(rc, "vrp_evaluate_records");
+}
+
+int vrp_decode_batch(vrp_instance_t h, const double *genes, int64_t gene_stride, int64_t N,
+                     int32_t relax, double penalty, double *fitness, double *makespan,
+                     int32_t *scheduled, int64_t *visits, void *ops_out, int32_t op_bytes,
+                     int64_t out_stride, int32_t *lens_out, void *stream) {
+    if (!h) return fail(VRP_EINVAL, "null instance%s");
+    if (N < 0 || (N > 0 && (!genes || !fitness))) return fail(VRP_EINVAL, "vrp_decode_batch: null buffer%s");
+    if (ops_out && op_bytes != 2 && op_bytes != 4) return fail(VRP_EINVAL, "op_bytes must be 2 or 4%s");
+    if (ops_out && out_stride < 2 * (int64_t)h->dev.n) return fail(VRP_EINVAL, "out_stride < 2n%s");
+    if (gene_stride < 4 * (int64_t)h->dev.n) return fail(VRP_EINVAL, "gene_stride < 4n%s");
+    if (N == 0) return 0;
+    int rc = launch_decode(h->dev, genes, gene_stride, N, relax, penalty, fitness, makespan, scheduled,
+                           visits, ops_out, ops_out ? op_bytes : 4, out_stride, lens_out,
+                           static_cast<cudaStream_t>(stream), h->sm_count);
+    return launch_result(rc, "vrp_decode_batch");
+}
+
+}  // extern "C"

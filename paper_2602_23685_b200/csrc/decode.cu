@@ -1,0 +1,329 @@
+// decode.cu -- K3: BRKGA multi-pass decoder (brkga.py:92-207) over a batch
+// of chromosomes, one warp per chromosome.
+//
+//  sort    stable argsort of the 2n priority genes (brkga.py:116): bitonic
+//          network in shared memory over (order-preserving u64 key, index)
+//          pairs -- a strict total order, hence equal to numpy's stable sort
+//          (-0.0 is canonicalised to +0.0, NaN sorts last as in numpy).
+//  decode  lane v = vehicle v holds (t, loc, net, lo, hi) in registers.  The
+//          pending list is scanned 32 ops at a time: a dropoff is deferred iff
+//          no vehicle can take one (the capacity test does not depend on the
+//          customer), a pickup iff its dropoff is unscheduled or no vehicle can
+//          take it -- so every lane classifies its own op with one shared-
+//          memory read, and the warp jumps straight to the first schedulable
+//          op (ballot + ffs), writing the deferred ones back in visit order
+//          (in place, stable).  The schedulable op is placed by the lanes in
+//          parallel: feasibility, completion max(t + d, ready), hint-first
+//          choice, else the lexicographic min of (completion, |v-hint|, v)
+//          via a butterfly reduction (brkga.py:149-176).
+//  emit    (op, vehicle) events are compacted vehicle-major with ballots.
+#include <float.h>
+#include <limits.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline int pow2_at_least(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+struct DecodeLayout {
+    int P2;
+    size_t keys, ready, seq_op, seq_v, idx, total;
+};
+
+// region K: sort keys during the sort, then {ready, seq_op, seq_v};
+// region I: sort indices, then the pending list (in place).
+__host__ __device__ inline DecodeLayout decode_layout(int n) {
+    DecodeLayout L;
+    const int two_n = 2 * n;
+    L.P2 = pow2_at_least(two_n);
+    L.keys = 0;
+    size_t after_sort = 0;
+    L.ready = after_sort; after_sort += align16(sizeof(double) * (size_t)(n + 1));
+    L.seq_op = after_sort; after_sort += align16(sizeof(uint16_t) * (size_t)two_n);
+    L.seq_v = after_sort; after_sort += align16((size_t)two_n);
+    size_t regionK = align16(sizeof(uint64_t) * (size_t)L.P2);
+    if (after_sort > regionK) regionK = after_sort;
+    L.idx = regionK;
+    L.total = regionK + align16(sizeof(uint16_t) * (size_t)L.P2);
+    return L;
+}
+
+__device__ __forceinline__ uint64_t order_key(double x) {
+    if (x != x) return 0xFFFFFFFFFFFFFFFEull;  // NaN: after every number
+    if (x == 0.0) x = 0.0;                    // -0.0 ties with +0.0
+    uint64_t b = (uint64_t)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// brkga.py:82-89 _hint_vehicle, with explicit round-to-nearest ops (no FMA)
+__device__ __forceinline__ int hint_vehicle(int m, double g) {
+    double x = __dmul_rn((double)m, g);
+    long long h = (long long)x;
+    if (__dsub_rn(x, (double)h) > 1.0 - 1e-9) h += 1;
+    return (int)(h < m ? h : m - 1);
+}
+
+__device__ __forceinline__ void bitonic_sort(uint64_t *key, uint16_t *idx, int P2, int lane) {
+    for (int k = 2; k <= P2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < (P2 >> 1); i += 32) {
+                int a = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+                int b = a + j;
+                uint64_t ka = key[a], kb = key[b];
+                uint16_t ia = idx[a], ib = idx[b];
+                bool a_gt_b = ka > kb || (ka == kb && ia > ib);
+                bool up = (a & k) == 0;
+                if (a_gt_b == up) {
+                    key[a] = kb; key[b] = ka;
+                    idx[a] = ib; idx[b] = ia;
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// warp-uniform: can any vehicle take a dropoff / a pickup now, and (strict
+// mode) the latest clock among vehicles that can take a pickup
+__device__ __forceinline__ void fleet_flags(bool vlane, double t, int net, int lo, int hi, int k,
+                                            int relax, bool &any_drop, bool &any_pick,
+                                            double &pick_maxT) {
+    int need = 1 - net, room = k - 1 - net;
+    bool cd = vlane && ((need > lo ? need : lo) <= hi);
+    bool cp = vlane && (lo <= (room < hi ? room : hi));
+    any_drop = __any_sync(VRP_FULL_MASK, cd);
+    any_pick = __any_sync(VRP_FULL_MASK, cp);
+    pick_maxT = relax ? 0.0 : warp_max(cp ? t : -DBL_MAX);
+}
+
+template <bool INTD, typename OutT>
+__global__ void __launch_bounds__(256, 1)
+decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, int64_t N,
+              int relax, double penalty, double *__restrict__ fitness_out,
+              double *__restrict__ makespan_out, int32_t *__restrict__ scheduled_out,
+              int64_t *__restrict__ visits_out, OutT *__restrict__ ops_out, int64_t ostride,
+              int32_t *__restrict__ lens_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    const int n = I.n, m = I.m, k = I.k, two_n = 2 * n;
+    const DecodeLayout Ly = decode_layout(n);
+    unsigned char *base = smem + (size_t)warp * Ly.total;
+    uint64_t *s_key = reinterpret_cast<uint64_t *>(base + Ly.keys);
+    volatile double *s_ready = reinterpret_cast<volatile double *>(base + Ly.ready);
+    uint16_t *s_seq_op = reinterpret_cast<uint16_t *>(base + Ly.seq_op);
+    uint8_t *s_seq_v = reinterpret_cast<uint8_t *>(base + Ly.seq_v);
+    uint16_t *s_pend = reinterpret_cast<uint16_t *>(base + Ly.idx);
+    const bool vlane = lane < m;
+    const unsigned lt = lanemask_lt();
+
+    for (int64_t chrom = (int64_t)blockIdx.x * wpb + warp; chrom < N;
+         chrom += (int64_t)gridDim.x * wpb) {
+        const double *g = genes + chrom * gstride;
+        // ---- stable argsort of the priorities
+        for (int i = lane; i < Ly.P2; i += 32) {
+            s_key[i] = i < two_n ? order_key(__ldg(g + i)) : ~0ull;
+            s_pend[i] = (uint16_t)i;
+        }
+        __syncwarp();
+        bitonic_sort(s_key, s_pend, Ly.P2, lane);
+        for (int c = lane; c <= n; c += 32) s_ready[c] = -1.0;  // -1: not dropped
+        __syncwarp();
+
+        // ---- vehicle state (lane v = vehicle v)
+        double t = 0.0;
+        int loc = 0, net = 0, lo = 0, hi = k, cnt = 0;
+        bool any_drop, any_pick;
+        double pick_maxT;
+        fleet_flags(vlane, t, net, lo, hi, k, relax, any_drop, any_pick, pick_maxT);
+
+        int npend = two_n, nseq = 0;
+        int64_t visits = 0;
+        for (int pass = 0; pass < two_n && npend; ++pass) {
+            visits += npend;
+            int nw = 0;
+            bool progressed = false;
+            for (int wbase = 0; wbase < npend; wbase += 32) {
+                const int j = wbase + lane;
+                const bool valid = j < npend;
+                const int op = valid ? s_pend[j] : 0;
+                const int c = op_customer(op);
+                const bool pk = op & 1;
+                unsigned todo = __ballot_sync(VRP_FULL_MASK, valid);
+                __syncwarp();
+                while (todo) {
+                    const double r = pk ? s_ready[c] : 0.0;
+                    const bool feas = pk ? (r >= 0.0 && any_pick && (relax || pick_maxT >= r)) : any_drop;
+                    const unsigned fm = __ballot_sync(VRP_FULL_MASK, feas) & todo;
+                    const unsigned defm = fm ? (todo & ((1u << (__ffs(fm) - 1)) - 1u)) : todo;
+                    if ((defm >> lane) & 1u) s_pend[nw + __popc(defm & lt)] = (uint16_t)op;
+                    nw += __popc(defm);
+                    if (!fm) break;
+                    const int f = __ffs(fm) - 1;
+                    todo &= ~((2u << f) - 1u);
+                    // ---- place op f (brkga.py:148-193)
+                    const int opf = __shfl_sync(VRP_FULL_MASK, op, f);
+                    const double rf = __shfl_sync(VRP_FULL_MASK, r, f);
+                    const int cf = op_customer(opf);
+                    const bool pickf = opf & 1;
+                    const double gene = __ldg(g + two_n + opf);
+                    double comp = 0.0;
+                    bool fv = false;
+                    if (vlane) {
+                        const double leg = dist<INTD>(I, loc, cf);
+                        const double arr = t + leg;
+                        if (pickf) {
+                            int room = k - 1 - net;
+                            bool cp = lo <= (room < hi ? room : hi);
+                            fv = cp && (relax || t >= rf);
+                            comp = relax ? (arr >= rf ? arr : rf) : arr;
+                        } else {
+                            int need = 1 - net;
+                            fv = (need > lo ? need : lo) <= hi;
+                            comp = arr;
+                        }
+                    }
+                    const int hint = hint_vehicle(m, gene);
+                    const unsigned fmask = __ballot_sync(VRP_FULL_MASK, fv);
+                    int vstar;
+                    if (hint >= 0 && hint < 32 && ((fmask >> hint) & 1u)) {
+                        vstar = hint;
+                    } else {
+                        double kc = fv ? comp : DBL_MAX;
+                        int kd = fv ? (lane > hint ? lane - hint : hint - lane) : INT_MAX;
+                        int kv = fv ? lane : INT_MAX;
+#pragma unroll
+                        for (int o = 16; o; o >>= 1) {
+                            double oc = __shfl_xor_sync(VRP_FULL_MASK, kc, o);
+                            int od = __shfl_xor_sync(VRP_FULL_MASK, kd, o);
+                            int ov = __shfl_xor_sync(VRP_FULL_MASK, kv, o);
+                            bool better = oc < kc || (oc == kc && (od < kd || (od == kd && ov < kv)));
+                            if (better) { kc = oc; kd = od; kv = ov; }
+                        }
+                        vstar = kv;
+                    }
+                    const double cstar = __shfl_sync(VRP_FULL_MASK, comp, vstar);
+                    if (lane == vstar) {
+                        t = cstar;
+                        loc = cf;
+                        if (pickf) { int room = k - 1 - net; hi = room < hi ? room : hi; ++net; }
+                        else { int need = 1 - net; lo = need > lo ? need : lo; --net; }
+                        ++cnt;
+                    }
+                    if (lane == 0) {
+                        if (!pickf) s_ready[cf] = cstar + __ldg(I.p + cf);
+                        s_seq_op[nseq] = (uint16_t)opf;
+                        s_seq_v[nseq] = (uint8_t)vstar;
+                    }
+                    ++nseq;
+                    progressed = true;
+                    fleet_flags(vlane, t, net, lo, hi, k, relax, any_drop, any_pick, pick_maxT);
+                    __syncwarp();
+                }
+                __syncwarp();
+            }
+            npend = nw;
+            if (!progressed) break;
+        }
+
+        // ---- fitness (brkga.py:198-200): unused vehicles return at 0 + d[0][0]
+        double ret = vlane ? t + dist<INTD>(I, loc, 0) : -DBL_MAX;
+        const double z = warp_max(ret);
+        if (lane == 0) {
+            fitness_out[chrom] = z + penalty * (double)npend;
+            if (makespan_out) makespan_out[chrom] = z;
+            if (scheduled_out) scheduled_out[chrom] = two_n - npend;
+            if (visits_out) visits_out[chrom] = visits;
+        }
+        // ---- emit the solution vehicle-major
+        if (ops_out) {
+            int off = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(VRP_FULL_MASK, off, o);
+                if (lane >= o) off += y;
+            }
+            off -= cnt;  // exclusive start of route `lane`
+            OutT *row = ops_out + chrom * ostride;
+            for (int sb = 0; sb < nseq; sb += 32) {
+                const int j = sb + lane;
+                const bool valid = j < nseq;
+                const int op = valid ? s_seq_op[j] : 0;
+                const int v = valid ? s_seq_v[j] : -1;
+                for (int u = 0; u < m; ++u) {
+                    const unsigned mk = __ballot_sync(VRP_FULL_MASK, v == u);
+                    const int ou = __shfl_sync(VRP_FULL_MASK, off, u);
+                    if (v == u) row[ou + __popc(mk & lt)] = (OutT)op;
+                    if (lane == u) off += __popc(mk);
+                }
+            }
+            for (int j = nseq + lane; j < two_n; j += 32) row[j] = (OutT)-1;
+            if (lens_out && vlane) lens_out[chrom * m + lane] = cnt;
+        }
+        __syncwarp();
+    }
+}
+
+template <bool INTD, typename OutT>
+int launch_t(const DevInstance &I, const double *genes, int64_t gstride, int64_t N, int relax,
+             double penalty, double *fitness, double *makespan, int32_t *scheduled, int64_t *visits,
+             void *ops_out, int64_t ostride, int32_t *lens_out, cudaStream_t stream, int sm_count) {
+    auto kern = decode_kernel<INTD, OutT>;
+    const size_t per_warp = decode_layout(I.n).total;
+    static size_t cached_pw = 0;
+    static int cached_w = 0, cached_blocks = 0;
+    if (cached_pw != per_warp) {
+        int best_w = 0, best_res = 0, best_blocks = 0;
+        for (int w = 8; w >= 1; w >>= 1) {
+            size_t bytes = per_warp * (size_t)w;
+            if (bytes > 227 * 1024) continue;
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+                return -1;
+            int blocks = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32 * w, bytes) != cudaSuccess)
+                return -1;
+            if (blocks * w > best_res) { best_res = blocks * w; best_w = w; best_blocks = blocks; }
+        }
+        if (!best_res) return -2;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per_warp * best_w));
+        cached_pw = per_warp; cached_w = best_w; cached_blocks = best_blocks;
+    }
+    const size_t bytes = per_warp * (size_t)cached_w;
+    int64_t want = (N + cached_w - 1) / cached_w;
+    int64_t grid = (int64_t)cached_blocks * sm_count;
+    if (grid > want) grid = want;
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, 32 * cached_w, bytes, stream>>>(I, genes, gstride, N, relax, penalty, fitness,
+                                                         makespan, scheduled, visits,
+                                                         static_cast<OutT *>(ops_out), ostride, lens_out);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace
+
+int launch_decode(const DevInstance &I, const double *genes, int64_t gstride, int64_t N, int relax,
+                  double penalty, double *fitness, double *makespan, int32_t *scheduled,
+                  int64_t *visits, void *ops_out, int op_bytes, int64_t ostride,
+                  int32_t *lens_out, cudaStream_t stream, int sm_count) {
+    if (op_bytes == 2) {
+        if (I.integral)
+            return launch_t<true, int16_t>(I, genes, gstride, N, relax, penalty, fitness, makespan,
+                                           scheduled, visits, ops_out, ostride, lens_out, stream, sm_count);
+        return launch_t<false, int16_t>(I, genes, gstride, N, relax, penalty, fitness, makespan,
+                                        scheduled, visits, ops_out, ostride, lens_out, stream, sm_count);
+    }
+    if (I.integral)
+        return launch_t<true, int32_t>(I, genes, gstride, N, relax, penalty, fitness, makespan,
+                                       scheduled, visits, ops_out, ostride, lens_out, stream, sm_count);
+    return launch_t<false, int32_t>(I, genes, gstride, N, relax, penalty, fitness, makespan,
+                                    scheduled, visits, ops_out, ostride, lens_out, stream, sm_count);
+}

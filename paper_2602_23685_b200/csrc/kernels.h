@@ -1,0 +1,18 @@
+// kernels.h -- host-side launchers implemented by the kernel translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+// makespan.cu (K1/K2); mode 0 exact, 1 evaluate, 2 two-pass; rec = event records
+int launch_makespan(const DevInstance &I, const void *ops, int op_bytes, int64_t stride,
+                    const int32_t *lens, int64_t N, int mode, bool rec, double *z, int32_t *status,
+                    double *returns, int32_t *bottleneck, double *arrival, double *timev,
+                    int32_t *q0, cudaStream_t stream, int sm_count);
+
+// decode.cu (K3)
+int launch_decode(const DevInstance &I, const double *genes, int64_t gstride, int64_t N, int relax,
+                  double penalty, double *fitness, double *makespan, int32_t *scheduled,
+                  int64_t *visits, void *ops_out, int op_bytes, int64_t ostride,
+                  int32_t *lens_out, cudaStream_t stream, int sm_count);

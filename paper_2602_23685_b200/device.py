@@ -1,0 +1,229 @@
+"""Device-resident instances and the batched entry points (torch tensors in,
+torch tensors out), all routed through the C-ABI of include/vrp_rpd.h.
+
+Batch layout (shared with the C-ABI and the oracle):
+  ops   int16|int32 [N, 2n]  op code 2(c-1)+kind, routes concatenated vehicle-major
+  lens  int32 [N, m]         route lengths
+  genes fp64  [N, 4n]        BRKGA chromosomes (priorities | hints)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+_HANDLES: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+class DeviceInstance:
+    """Owns the device copy of an instance (d fp64 + int32 twin, p) on the
+    current CUDA device.  Create via :func:`device_instance`."""
+
+    def __init__(self, n: int, m: int, k: int, d: np.ndarray, p: np.ndarray):
+        L = N.lib()
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        if d.shape != (n + 1, n + 1) or p.shape != (n + 1,):
+            raise ValueError("d must be (n+1)x(n+1) and p (n+1)")
+        h = C.c_void_p()
+        N.check(L.vrp_instance_create(n, m, k, d.ctypes.data_as(C.c_void_p),
+                                      p.ctypes.data_as(C.c_void_p), C.byref(h)),
+                "vrp_instance_create")
+        self._h = h
+        self.n, self.m, self.k = n, m, k
+        self.device = torch.cuda.current_device()
+        integral = C.c_int32()
+        N.check(L.vrp_instance_info(h, None, None, None, C.byref(integral)))
+        self.integral = bool(integral.value)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and N._lib is not None:
+            try:
+                N._lib.vrp_instance_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+            self._h = None
+
+
+def device_instance(instance) -> DeviceInstance:
+    """Cached DeviceInstance for an ``Instance`` (or anything with n,m,k,d,p)."""
+    N.lib()  # raises NativeUnavailable without the library or a device
+    dev = torch.cuda.current_device()
+    cache = getattr(instance, "_cache", None)
+    key = ("device_instance", dev)
+    if cache is not None and key in cache:
+        return cache[key]
+    if hasattr(instance, "arrays"):
+        d, p = instance.arrays()
+    else:
+        d, p = np.asarray(instance.d, np.float64), np.asarray(instance.p, np.float64)
+    di = DeviceInstance(int(instance.n), int(instance.m), int(instance.k), d, p)
+    if cache is not None:
+        cache[key] = di
+    return di
+
+
+def _cuda(t, dtype=None):
+    t = torch.as_tensor(t)
+    if dtype is not None and t.dtype != dtype:
+        t = t.to(dtype)
+    if not t.is_cuda:
+        t = t.cuda()
+    return t.contiguous()
+
+
+def makespan_batch(instance, ops, lens, mode: int = N.MODE_EXACT, want_returns: bool = False,
+                   want_bottleneck: bool = False, stream=None, out=None):
+    """Score a batch of candidates on the GPU (K1/K2).
+
+    ``mode``: 0 exact_makespan, 1 evaluate (validating), 2 two_pass_estimate.
+    Returns dict of device tensors: z fp64 [N], status int32 [N] (+ returns
+    fp64 [N, m], bottleneck int32 [N])."""
+    di = device_instance(instance)
+    ops = _cuda(ops)
+    if ops.dtype not in (torch.int16, torch.int32):
+        ops = ops.to(torch.int32)
+    lens = _cuda(lens, torch.int32)
+    if ops.dim() == 1:
+        ops = ops.unsqueeze(0)
+    if lens.dim() == 1:
+        lens = lens.unsqueeze(0)
+    Nc = ops.shape[0]
+    if lens.shape != (Nc, di.m):
+        raise ValueError(f"lens must be [N, m={di.m}], got {tuple(lens.shape)}")
+    dev = ops.device
+    res = out if out is not None else {}
+    if "z" not in res:
+        res["z"] = torch.empty(Nc, dtype=torch.float64, device=dev)
+        res["status"] = torch.empty(Nc, dtype=torch.int32, device=dev)
+    if want_returns and "returns" not in res:
+        res["returns"] = torch.empty((Nc, di.m), dtype=torch.float64, device=dev)
+    if want_bottleneck and "bottleneck" not in res:
+        res["bottleneck"] = torch.empty(Nc, dtype=torch.int32, device=dev)
+    L = N.lib()
+    N.check(L.vrp_makespan_batch(di.handle, N.ptr(ops), ops.element_size(), ops.stride(0),
+                                 N.ptr(lens), Nc, int(mode), N.ptr(res["z"]), N.ptr(res["status"]),
+                                 N.ptr(res.get("returns")), N.ptr(res.get("bottleneck")),
+                                 N.stream_handle(stream)), "vrp_makespan_batch")
+    return res
+
+
+def evaluate_records(instance, ops, lens, stream=None):
+    """Full evaluate records (arrival/time per op, q0 per vehicle) for a batch."""
+    di = device_instance(instance)
+    ops = _cuda(ops, torch.int32)
+    lens = _cuda(lens, torch.int32)
+    if ops.dim() == 1:
+        ops, lens = ops.unsqueeze(0), lens.unsqueeze(0)
+    Nc = ops.shape[0]
+    dev = ops.device
+    res = {"z": torch.empty(Nc, dtype=torch.float64, device=dev),
+           "status": torch.empty(Nc, dtype=torch.int32, device=dev),
+           "returns": torch.empty((Nc, di.m), dtype=torch.float64, device=dev),
+           "arrival": torch.zeros(ops.shape, dtype=torch.float64, device=dev),
+           "time": torch.zeros(ops.shape, dtype=torch.float64, device=dev),
+           "q0": torch.zeros((Nc, di.m), dtype=torch.int32, device=dev)}
+    N.check(N.lib().vrp_evaluate_records(di.handle, N.ptr(ops), ops.stride(0), N.ptr(lens), Nc,
+                                         N.ptr(res["z"]), N.ptr(res["status"]),
+                                         N.ptr(res["returns"]), N.ptr(res["arrival"]),
+                                         N.ptr(res["time"]), N.ptr(res["q0"]),
+                                         N.stream_handle(stream)), "vrp_evaluate_records")
+    return res
+
+
+def decode_batch(instance, genes, relax: bool = True, penalty: float = 1e6,
+                 want_solution: bool = True, op_dtype=torch.int32, stream=None, out=None):
+    """BRKGA decode (K3) of genes [N, 4n] fp64 on the GPU.
+
+    Returns dict of device tensors: fitness, makespan, scheduled, visits and,
+    if ``want_solution``, ops [N, 2n] (vehicle-major, -1 padded) and lens [N, m]."""
+    di = device_instance(instance)
+    genes = _cuda(genes, torch.float64)
+    if genes.dim() == 1:
+        genes = genes.unsqueeze(0)
+    Nc = genes.shape[0]
+    if genes.shape[1] < 4 * di.n:
+        raise ValueError(f"chromosomes need 4n = {4 * di.n} genes")
+    dev = genes.device
+    res = out if out is not None else {}
+    if "fitness" not in res:
+        res["fitness"] = torch.empty(Nc, dtype=torch.float64, device=dev)
+        res["makespan"] = torch.empty(Nc, dtype=torch.float64, device=dev)
+        res["scheduled"] = torch.empty(Nc, dtype=torch.int32, device=dev)
+        res["visits"] = torch.empty(Nc, dtype=torch.int64, device=dev)
+    if want_solution and "ops" not in res:
+        res["ops"] = torch.empty((Nc, 2 * di.n), dtype=op_dtype, device=dev)
+        res["lens"] = torch.empty((Nc, di.m), dtype=torch.int32, device=dev)
+    ops = res.get("ops") if want_solution else None
+    N.check(N.lib().vrp_decode_batch(
+        di.handle, N.ptr(genes), genes.stride(0), Nc, int(bool(relax)), float(penalty),
+        N.ptr(res["fitness"]), N.ptr(res["makespan"]), N.ptr(res["scheduled"]),
+        N.ptr(res["visits"]), N.ptr(ops), ops.element_size() if ops is not None else 4,
+        ops.stride(0) if ops is not None else 2 * di.n,
+        N.ptr(res.get("lens") if want_solution else None), N.stream_handle(stream)),
+        "vrp_decode_batch")
+    return res
+
+
+_PIPE = {}
+
+
+def _pipeline(di, chunk: int, op_dtype):
+    key = (id(di), torch.cuda.current_device(), chunk, op_dtype)
+    st = _PIPE.get(key)
+    if st is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        st = {"streams": [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)],
+              "bufs": [{"ops": torch.empty((chunk, 2 * di.n), dtype=op_dtype, device=dev),
+                        "lens": torch.empty((chunk, di.m), dtype=torch.int32, device=dev),
+                        "z": torch.empty(chunk, dtype=torch.float64, device=dev),
+                        "status": torch.empty(chunk, dtype=torch.int32, device=dev)}
+                       for _ in range(2)]}
+        _PIPE[key] = st
+    return st
+
+
+def score_host_batch(instance, ops, lens, mode: int = N.MODE_EXACT, chunk: int = 1 << 16):
+    """End-to-end scoring of HOST candidates: chunks are copied host->device,
+    scored by K1/K2 and their (z, status) copied back, alternating two CUDA
+    streams so the PCIe transfers overlap the kernel.  ``ops``/``lens`` should
+    be pinned CPU tensors (numpy arrays are pinned on the fly).  Returns numpy
+    (z, status)."""
+    di = device_instance(instance)
+    if not isinstance(ops, torch.Tensor):
+        ops = torch.from_numpy(np.ascontiguousarray(ops)).pin_memory()
+    if not isinstance(lens, torch.Tensor):
+        lens = torch.from_numpy(np.ascontiguousarray(lens, dtype=np.int32)).pin_memory()
+    if ops.dtype not in (torch.int16, torch.int32):
+        ops = ops.to(torch.int32)
+    Nc = ops.shape[0]
+    z = torch.empty(Nc, dtype=torch.float64, pin_memory=True)
+    status = torch.empty(Nc, dtype=torch.int32, pin_memory=True)
+    st = _pipeline(di, chunk, ops.dtype)
+    cur = torch.cuda.current_stream()
+    for s in st["streams"]:
+        s.wait_stream(cur)
+    for i, a in enumerate(range(0, Nc, chunk)):
+        b = min(Nc, a + chunk)
+        c = b - a
+        s, buf = st["streams"][i & 1], st["bufs"][i & 1]
+        with torch.cuda.stream(s):
+            buf["ops"][:c].copy_(ops[a:b], non_blocking=True)
+            buf["lens"][:c].copy_(lens[a:b], non_blocking=True)
+            out = {"z": buf["z"][:c], "status": buf["status"][:c]}
+            makespan_batch(instance, buf["ops"][:c], buf["lens"][:c], mode=mode, stream=s, out=out)
+            z[a:b].copy_(buf["z"][:c], non_blocking=True)
+            status[a:b].copy_(buf["status"][:c], non_blocking=True)
+    for s in st["streams"]:
+        cur.wait_stream(s)
+    cur.synchronize()
+    return z.numpy(), status.numpy()

@@ -1,0 +1,70 @@
+"""CPU-side checks of the C-ABI boundary: the library builds for sm_100a,
+loads, and exports every entry point include/vrp_rpd.h declares; the product
+path refuses to run without a GPU (no CPU fallback)."""
+import ctypes
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2602_23685_b200 import _native
+from paper_2602_23685_b200 import build as B
+
+REPO = Path(__file__).resolve().parent.parent
+HEADER = REPO / "include" / "vrp_rpd.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^(?:int|const char \*)\s*(vrp_\w+)\s*\(", text, re.M)))
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    return B.build()
+
+
+def test_header_declares_entry_points():
+    syms = declared_symbols()
+    assert "vrp_makespan_batch" in syms and "vrp_decode_batch" in syms
+    assert len(syms) >= 8
+
+
+def test_library_exports_every_declared_symbol(libpath):
+    out = subprocess.run(["nm", "-D", "--defined-only", str(libpath)], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (vrp_\w+)", out))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, f"declared but not exported: {missing}"
+
+
+def test_library_is_sm100a(libpath):
+    out = subprocess.run(["cuobjdump", "--list-elf", str(libpath)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_library_loads_and_reports_version(libpath):
+    L = _native.lib(require_device=False)
+    abi, arch = ctypes.c_int32(), ctypes.c_int32()
+    assert L.vrp_version(ctypes.byref(abi), ctypes.byref(arch)) == 0
+    assert abi.value >= 1 and arch.value == 1000
+
+
+def test_null_arguments_are_rejected_without_device(libpath):
+    L = _native.lib(require_device=False)
+    rc = L.vrp_makespan_batch(None, None, 4, 0, None, 1, 0, None, None, None, None, None)
+    assert rc == 1
+    assert b"null" in L.vrp_last_error()
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_product_path_fails_loudly_without_gpu():
+    from paper_2602_23685_b200.instance import FleetConfig, Instance
+    from paper_2602_23685_b200.schedule import Solution, exact_makespan
+    inst = Instance(n=1, d=((0, 10), (10, 0)), p=(0, 20), fleet=FleetConfig(1, 1), label="t")
+    with pytest.raises(_native.NativeUnavailable):
+        exact_makespan(inst, Solution.from_lists([[(1, "D"), (1, "P")]]))

@@ -1,0 +1,131 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the reference's
+golden vectors and the CPU oracle -- bit-exact (integer configs and the
+non-integer ones alike, since the kernels keep the reference's fp64 order)."""
+import numpy as np
+import pytest
+import torch
+
+import inputs as I
+from conftest import CONFIG_KEYS, config_instance
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+CID = {"gr17": 1, "eil51": 2, "kroA100": 3, "a280": 4, "dsj1000": 5}
+MODES = ((0, "exact"), (1, "eval"), (2, "two"))
+
+
+def dev():
+    from paper_2602_23685_b200 import device
+    return device
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("key", CONFIG_KEYS)
+@pytest.mark.parametrize("tag", ["dec", "rnd", "blk", "swp", "mal"])
+@pytest.mark.parametrize("op_dtype", [np.int32, np.int16])
+def test_makespan_family_vs_golden(key, tag, op_dtype, golden):
+    inst = config_instance(key)
+    pre = f"{key}/"
+    ops = golden[pre + ("dec_ops" if tag == "dec" else f"{tag}_ops")].astype(op_dtype)
+    lens = golden[pre + ("dec_lens" if tag in ("dec", "swp") else f"{tag}_lens")]
+    for mode, short in MODES:
+        if tag == "mal" and mode == 0:
+            continue  # exact_makespan does not validate; its result on malformed input is loop-order dependent
+        r = dev().makespan_batch(inst, _cuda(ops), _cuda(lens), mode=mode, want_returns=True)
+        st = r["status"].cpu().numpy()
+        np.testing.assert_array_equal(st, golden[pre + f"{tag}_st_{short}"], err_msg=short)
+        np.testing.assert_array_equal(r["z"].cpu().numpy(), golden[pre + f"{tag}_z_{short}"], err_msg=short)
+        if mode == 1:
+            ok = st == 0
+            np.testing.assert_array_equal(r["returns"].cpu().numpy()[ok],
+                                          golden[pre + f"{tag}_returns"][ok])
+
+
+@pytest.mark.parametrize("key", CONFIG_KEYS)
+@pytest.mark.parametrize("tag", ["dec", "enc", "strict"])
+def test_decode_vs_golden(key, tag, golden):
+    inst = config_instance(key)
+    pre = f"{key}/"
+    n_dec = golden[pre + "dec_ops"].shape[0]
+    genes = I.chromosomes(inst.n, n_dec, (136, CID[key]))
+    if tag == "enc":
+        genes = golden[pre + "enc_genes"]
+    elif tag == "strict":
+        genes = genes[: golden[pre + "enc_genes"].shape[0]]
+    r = dev().decode_batch(inst, _cuda(genes), relax=(tag != "strict"))
+    np.testing.assert_array_equal(r["ops"].cpu().numpy(), golden[pre + f"{tag}_ops"])
+    np.testing.assert_array_equal(r["lens"].cpu().numpy(), golden[pre + f"{tag}_lens"])
+    for f in ("fitness", "makespan", "scheduled", "visits"):
+        np.testing.assert_array_equal(r[f].cpu().numpy(), golden[pre + f"{tag}_{f}"], err_msg=f)
+
+
+@pytest.mark.parametrize("key,count", [("gr17", 4096), ("eil51", 2048), ("kroA100", 1024),
+                                       ("a280", 512), ("dsj1000", 256)])
+def test_decode_then_score_vs_oracle_at_scale(key, count):
+    """Fresh chromosomes (not in the golden set): GPU decode == oracle decode,
+    and the decoded makespan equals exact_makespan of the decoded solution
+    (SURVEY Appendix A.16 cross-check), int16 and int32 op paths alike."""
+    inst = config_instance(key)
+    genes = I.chromosomes(inst.n, count, (999, CID[key]))
+    g = _cuda(genes)
+    r = dev().decode_batch(inst, g)
+    ref = O.decode_batch(inst, genes)
+    np.testing.assert_array_equal(r["ops"].cpu().numpy(), ref["ops"])
+    np.testing.assert_array_equal(r["fitness"].cpu().numpy(), ref["fitness"])
+    np.testing.assert_array_equal(r["visits"].cpu().numpy(), ref["visits"])
+    r16 = dev().decode_batch(inst, g, op_dtype=torch.int16)
+    assert torch.equal(r16["ops"].to(torch.int32), r["ops"])
+    for ops in (r["ops"], r16["ops"]):
+        s = dev().makespan_batch(inst, ops, r["lens"], mode=0)
+        assert (s["status"] == 0).all()
+        assert torch.equal(s["z"], r["makespan"])
+    z2, st2 = O.makespan_batch(inst, ref["ops"], ref["lens"], mode="two_pass")
+    s2 = dev().makespan_batch(inst, r["ops"], r["lens"], mode=2)
+    np.testing.assert_array_equal(s2["status"].cpu().numpy(), st2)
+    np.testing.assert_array_equal(s2["z"].cpu().numpy(), z2)
+
+
+@pytest.mark.parametrize("key", ["gr17", "a280"])
+def test_evaluate_records_vs_oracle(key, golden):
+    inst = config_instance(key)
+    ops = golden[f"{key}/dec_ops"][:8]
+    lens = golden[f"{key}/dec_lens"][:8]
+    r = dev().evaluate_records(inst, _cuda(ops), _cuda(lens))
+    for i in range(ops.shape[0]):
+        st, z, ret, arr, tim, q0 = O.evaluate_one(inst, ops[i], lens[i])
+        assert int(r["status"][i]) == st == 0
+        assert float(r["z"][i]) == z
+        np.testing.assert_array_equal(r["arrival"][i].cpu().numpy(), arr)
+        np.testing.assert_array_equal(r["time"][i].cpu().numpy(), tim)
+        np.testing.assert_array_equal(r["q0"][i].cpu().numpy(), q0)
+
+
+def test_non_integral_instance_bit_exact():
+    """fp64 path (no int32 twin): perturbed non-integer d and p."""
+    from paper_2602_23685_b200.instance import Instance
+    base = config_instance("kroA100")
+    d, p = base.arrays()
+    rng = np.random.default_rng(5)
+    d2 = d + rng.random(d.shape) * 0.37
+    d2 = (d2 + d2.T) / 2
+    np.fill_diagonal(d2, 0.0)
+    p2 = p * 1.0001 + rng.random(p.shape) / 3
+    p2[0] = 0.0
+    inst = Instance.from_arrays(d2, p2, base.m, base.k, label="kro-frac")
+    genes = I.chromosomes(inst.n, 256, (5, 5))
+    r = dev().decode_batch(inst, _cuda(genes))
+    ref = O.decode_batch(inst, genes)
+    np.testing.assert_array_equal(r["ops"].cpu().numpy(), ref["ops"])
+    np.testing.assert_array_equal(r["fitness"].cpu().numpy(), ref["fitness"])
+    ops, lens = I.random_candidates(inst.n, inst.m, 64, (5, 6))
+    ops = np.concatenate([ref["ops"], ops, I.swap_perturb(ref["ops"], ref["lens"], (5, 7))])
+    lens = np.concatenate([ref["lens"], lens, ref["lens"]])
+    for mode, name in ((0, "exact"), (1, "evaluate"), (2, "two_pass")):
+        s = dev().makespan_batch(inst, _cuda(ops), _cuda(lens), mode=mode)
+        z, st = O.makespan_batch(inst, ops, lens, mode=name)
+        np.testing.assert_array_equal(s["status"].cpu().numpy(), st)
+        np.testing.assert_array_equal(s["z"].cpu().numpy(), z)
