@@ -12,6 +12,7 @@ struct vrp_instance {
     double *d = nullptr;
     int32_t *d32 = nullptr;
     double *p = nullptr;
+    int32_t *p32 = nullptr;
     int device = 0;
     int sm_count = 148;
 };
@@ -61,6 +62,10 @@ int vrp_instance_create(int32_t n, int32_t m, int32_t k, const double *d_host, c
         if (!(x >= 0.0 && x < 2147483648.0 && x == std::floor(x))) integral = false;
         if (std::signbit(x)) integral = false;  // keep -0.0 bit-exact in the fp64 table
     }
+    for (int32_t i = 0; i <= n && integral; ++i) {
+        double x = p_host[i];
+        if (!(x >= 0.0 && x < 2147483648.0 && x == std::floor(x)) || std::signbit(x)) integral = false;
+    }
     vrp_instance *h = new (std::nothrow) vrp_instance();
     if (!h) return fail(VRP_EINVAL, "out of host memory%s");
     cudaError_t e = cudaGetDevice(&h->device);
@@ -75,6 +80,9 @@ int vrp_instance_create(int32_t n, int32_t m, int32_t k, const double *d_host, c
         for (size_t i = 0; i < cells; ++i) tmp[i] = (int32_t)d_host[i];
         e = cudaMalloc(&h->d32, cells * sizeof(int32_t));
         if (e == cudaSuccess) e = cudaMemcpy(h->d32, tmp, cells * sizeof(int32_t), cudaMemcpyHostToDevice);
+        for (int32_t i = 0; i <= n; ++i) tmp[i] = (int32_t)p_host[i];
+        if (e == cudaSuccess) e = cudaMalloc(&h->p32, (size_t)(n + 1) * sizeof(int32_t));
+        if (e == cudaSuccess) e = cudaMemcpy(h->p32, tmp, (size_t)(n + 1) * sizeof(int32_t), cudaMemcpyHostToDevice);
         delete[] tmp;
     }
     if (e != cudaSuccess) {
@@ -82,7 +90,7 @@ int vrp_instance_create(int32_t n, int32_t m, int32_t k, const double *d_host, c
         return cuda_fail(e, "vrp_instance_create");
     }
     h->dev.n = n; h->dev.m = m; h->dev.k = k; h->dev.W = n + 1;
-    h->dev.d = h->d; h->dev.d32 = h->d32; h->dev.p = h->p;
+    h->dev.d = h->d; h->dev.d32 = h->d32; h->dev.p = h->p; h->dev.p32 = h->p32;
     h->dev.integral = integral ? 1 : 0;
     *out = h;
     return 0;
@@ -93,6 +101,7 @@ int vrp_instance_destroy(vrp_instance_t h) {
     if (h->d) cudaFree(h->d);
     if (h->d32) cudaFree(h->d32);
     if (h->p) cudaFree(h->p);
+    if (h->p32) cudaFree(h->p32);
     delete h;
     return 0;
 }

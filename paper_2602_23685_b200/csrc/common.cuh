@@ -11,7 +11,8 @@ struct DevInstance {
     const double *d;          // (n+1)^2 fp64
     const int32_t *d32;       // same values as int32 when `integral`, else null
     const double *p;          // n+1 fp64
-    int32_t integral;
+    const int32_t *p32;       // same values as int32 when `integral`, else null
+    int32_t integral;         // every d and p entry is an integer in [0, 2^31)
 };
 
 // op code = 2*(c-1) + kind  (brkga.py:73-75)

@@ -283,7 +283,7 @@ int launch_t(const DevInstance &I, const double *genes, int64_t gstride, int64_t
     static int cached_w = 0, cached_blocks = 0;
     if (cached_pw != per_warp) {
         int best_w = 0, best_res = 0, best_blocks = 0;
-        for (int w = 8; w >= 1; w >>= 1) {
+        for (int w = 8; w >= 1; --w) {
             size_t bytes = per_warp * (size_t)w;
             if (bytes > 227 * 1024) continue;
             if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)

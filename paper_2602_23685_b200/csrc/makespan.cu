@@ -31,6 +31,7 @@ namespace {
 constexpr int MODE_EXACT = 0, MODE_EVAL = 1, MODE_TWO = 2;
 constexpr uint16_t START_BIT = 0x8000;  // marks the first op of a route in s_op
 constexpr int ST_OK = 0, ST_CAP = 1, ST_DEAD = 2, ST_MAL = 3;
+constexpr int GATHER_BATCH = 16;         // independent L2 gathers in flight per lane
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -39,6 +40,7 @@ struct LegType { using T = double; };
 template <>
 struct LegType<true> { using T = int32_t; };
 
+// Per-warp shared-memory slots (one candidate in flight per warp) ...
 struct WarpLayout {
     size_t ready, leg, op, posd, total;
 };
@@ -52,6 +54,11 @@ __host__ __device__ inline WarpLayout warp_layout(int n, bool intd, int mode) {
     L.posd = o;  if (mode == MODE_TWO) o += align16(sizeof(uint16_t) * (size_t)(n + 1));
     L.total = o;
     return L;
+}
+
+// ... plus one block-shared copy of p (processing times), read on every dropoff.
+__host__ __device__ inline size_t block_p_bytes(int n, bool intd) {
+    return align16((intd ? 4 : 8) * (size_t)(n + 1));
 }
 
 __device__ __forceinline__ void cap_step(int op, int k, int &s, int &lo, int &hi) {
@@ -73,13 +80,18 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     const int wpb = blockDim.x >> 5;
     const int n = I.n, m = I.m, k = I.k, two_n = 2 * n;
     const WarpLayout Lw = warp_layout(n, INTD, MODE);
-    unsigned char *base = smem + (size_t)warp * Lw.total;
-    volatile double *s_ready = reinterpret_cast<volatile double *>(base + Lw.ready);
+    LegT *s_p = reinterpret_cast<LegT *>(smem);
+    unsigned char *base = smem + block_p_bytes(n, INTD) + (size_t)warp * Lw.total;
+    double *s_ready = reinterpret_cast<double *>(base + Lw.ready);
     uint32_t *s_bits = reinterpret_cast<uint32_t *>(base + Lw.ready);  // validation bitmap (aliases ready)
     LegT *s_leg = reinterpret_cast<LegT *>(base + Lw.leg);
     uint16_t *s_op = reinterpret_cast<uint16_t *>(base + Lw.op);
     uint16_t *s_posd = reinterpret_cast<uint16_t *>(base + Lw.posd);
     const bool vlane = lane < m;
+
+    for (int c = threadIdx.x; c <= n; c += blockDim.x)
+        s_p[c] = INTD ? (LegT)__ldg(I.p32 + c) : (LegT)__ldg(I.p + c);
+    __syncthreads();
 
     for (int64_t cand = (int64_t)blockIdx.x * wpb + warp; cand < N;
          cand += (int64_t)gridDim.x * wpb) {
@@ -97,13 +109,14 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         bool bad = __any_sync(VRP_FULL_MASK, L < 0) || total > two_n ||
                    (MODE != MODE_EXACT && total != two_n) || total > stride;
 
-        // ---- stage ops
+        // ---- stage ops (streaming loads) + validation
         if (MODE != MODE_EXACT && !bad) {
             for (int w = lane; w < (two_n + 31) / 32; w += 32) s_bits[w] = 0u;
             __syncwarp();
         }
         if (!bad) {
             bool mine_bad = false;
+#pragma unroll 4
             for (int j = lane; j < total; j += 32) {
                 int op = (int)load_stream(row + j);
                 if (op < 0 || op >= two_n) { mine_bad = true; op = 0; }
@@ -123,22 +136,38 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 if (bottleneck_out) bottleneck_out[cand] = 0;
             }
             if (returns_out && vlane) returns_out[cand * m + lane] = 0.0;
+            __syncwarp();
             continue;
         }
         __syncwarp();
         if (vlane && L > 0) s_op[off] |= START_BIT;
         __syncwarp();
 
-        // ---- gather legs (independent of times: full MLP), init ready table
-        for (int j = lane; j < total; j += 32) {
-            int raw = s_op[j];
-            int c = op_customer(raw & 0x7fff);
-            int prev = (raw & START_BIT) ? 0 : op_customer(s_op[j - 1] & 0x7fff);
-            if (INTD) s_leg[j] = (LegT)__ldg(I.d32 + (int64_t)prev * I.W + c);
-            else s_leg[j] = (LegT)__ldg(I.d + (int64_t)prev * I.W + c);
-            if (MODE == MODE_TWO && !(raw & 1)) s_posd[c] = (uint16_t)j;
+        // ---- gather legs d[prev][c]: independent of all times, so issue
+        // GATHER_BATCH loads per lane before consuming any of them
+        for (int j0 = lane; j0 < total; j0 += 32 * GATHER_BATCH) {
+            int64_t addr[GATHER_BATCH];
+#pragma unroll
+            for (int u = 0; u < GATHER_BATCH; ++u) {
+                const int j = j0 + 32 * u;
+                addr[u] = 0;
+                if (j < total) {
+                    const int raw = s_op[j];
+                    const int c = op_customer(raw & 0x7fff);
+                    const int prev = (raw & START_BIT) ? 0 : op_customer(s_op[j - 1] & 0x7fff);
+                    addr[u] = (int64_t)prev * I.W + c;
+                    if (MODE == MODE_TWO && !(raw & 1)) s_posd[c] = (uint16_t)j;
+                }
+            }
+            LegT v[GATHER_BATCH];
+#pragma unroll
+            for (int u = 0; u < GATHER_BATCH; ++u)
+                v[u] = INTD ? (LegT)__ldg(I.d32 + addr[u]) : (LegT)__ldg(I.d + addr[u]);
+#pragma unroll
+            for (int u = 0; u < GATHER_BATCH; ++u)
+                if (j0 + 32 * u < total) s_leg[j0 + 32 * u] = v[u];
         }
-        for (int c = lane; c <= n; c += 32) s_ready[c] = -1.0;
+        for (int c = lane; c <= n; c += 32) s_ready[c] = -1.0;  // -1: dropoff not done
         __syncwarp();
 
         const int end = off + L;
@@ -150,12 +179,12 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             // same-route pickup before its own dropoff => Deadlock (:362-369)
             if (vlane) {
                 for (int i = off; i < end; ++i) {
-                    int op = s_op[i] & 0x7fff;
-                    int c = op_customer(op);
+                    const int op = s_op[i] & 0x7fff;
+                    const int c = op_customer(op);
                     t = t + (double)s_leg[i];
-                    if (!(op & 1)) s_ready[c] = t + __ldg(I.p + c);
+                    if (!(op & 1)) s_ready[c] = t + (double)s_p[c];
                     else {
-                        int pd = s_posd[c];
+                        const int pd = s_posd[c];
                         if (pd > i && pd < end) dead = true;
                     }
                     cap_step(op, k, s, lo, hi);
@@ -167,31 +196,34 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             t = 0.0;
             if (vlane && !dead) {
                 for (int i = off; i < end; ++i) {
-                    int op = s_op[i] & 0x7fff;
+                    const int op = s_op[i] & 0x7fff;
                     t = t + (double)s_leg[i];
                     if (op & 1) {
-                        double r = s_ready[op_customer(op)];
+                        const double r = s_ready[op_customer(op)];
                         if (r > t) t = r;
                     }
                 }
             }
         } else {
+            // event replay in rounds; values written by other lanes become
+            // visible at the __syncwarp() closing each round, a lane that reads
+            // an unset ready[c] simply stops and resumes next round
             int i = off;
             for (;;) {
                 const int i0 = i;
                 if (vlane) {
                     while (i < end) {
-                        int op = s_op[i] & 0x7fff;
-                        int c = op_customer(op);
-                        double lg = (double)s_leg[i];
+                        const int op = s_op[i] & 0x7fff;
+                        const int c = op_customer(op);
+                        const double lg = (double)s_leg[i];
                         if (!(op & 1)) {
                             t = t + lg;
-                            s_ready[c] = t + __ldg(I.p + c);
+                            s_ready[c] = t + (double)s_p[c];
                             if (REC) { arrival_out[cand * stride + i] = t; time_out[cand * stride + i] = t; }
                         } else {
-                            double r = s_ready[c];
+                            const double r = s_ready[c];
                             if (r < 0.0) break;  // dropoff not performed yet
-                            double arr = t + lg;
+                            const double arr = t + lg;
                             t = arr >= r ? arr : r;
                             if (REC) { arrival_out[cand * stride + i] = arr; time_out[cand * stride + i] = t; }
                         }
@@ -208,14 +240,14 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 for (int j = i; j < end; ++j) cap_step(s_op[j] & 0x7fff, k, s, lo, hi);
         }
         const bool capfail = __any_sync(VRP_FULL_MASK, vlane && lo > hi);
-        int st = capfail ? ST_CAP : (dead ? ST_DEAD : ST_OK);
+        const int st = capfail ? ST_CAP : (dead ? ST_DEAD : ST_OK);
 
         double ret = 0.0;
         if (st == ST_OK && vlane && L > 0)
             ret = t + dist<INTD>(I, op_customer(s_op[end - 1] & 0x7fff), 0);
         double z = warp_max(ret);  // returns are >= 0; empty routes count as 0
         if (st != ST_OK) z = 0.0;
-        unsigned bmask = __ballot_sync(VRP_FULL_MASK, vlane && ret == z);
+        const unsigned bmask = __ballot_sync(VRP_FULL_MASK, vlane && ret == z);
         if (lane == 0) {
             z_out[cand] = z;
             status_out[cand] = st;
@@ -233,14 +265,16 @@ int launch_t(const DevInstance &I, const void *ops, int64_t stride, const int32_
              double *arrival, double *timev, int32_t *q0, cudaStream_t stream, int sm_count) {
     auto kern = makespan_kernel<OpT, INTD, MODE, REC>;
     const size_t per_warp = warp_layout(I.n, INTD, MODE).total;
+    const size_t shared_p = block_p_bytes(I.n, INTD);
     // choose warps/block maximising resident warps per SM under the smem
     // budget; cached per instantiation for the last per-warp footprint
     static size_t cached_pw = 0;
     static int cached_w = 0, cached_blocks = 0;
     int best_w = 1, best_res = 0, best_blocks = 1;
-    if (cached_pw == per_warp) { best_w = cached_w; best_blocks = cached_blocks; best_res = 1; }
-    for (int w = 8; w >= 1 && !best_res; w >>= 1) {
-        size_t bytes = per_warp * (size_t)w;
+    const bool hit = cached_pw == per_warp;
+    if (hit) { best_w = cached_w; best_blocks = cached_blocks; best_res = 1; }
+    for (int w = 8; w >= 1 && !hit; --w) {
+        size_t bytes = shared_p + per_warp * (size_t)w;
         if (bytes > 227 * 1024) continue;
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
             return -1;
@@ -250,7 +284,7 @@ int launch_t(const DevInstance &I, const void *ops, int64_t stride, const int32_
         if (blocks * w > best_res) { best_res = blocks * w; best_w = w; best_blocks = blocks; }
     }
     if (best_res == 0) return -2;
-    size_t bytes = per_warp * (size_t)best_w;
+    size_t bytes = shared_p + per_warp * (size_t)best_w;
     if (cached_pw != per_warp) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
         cached_pw = per_warp; cached_w = best_w; cached_blocks = best_blocks;

@@ -72,6 +72,11 @@ def device_instance(instance) -> DeviceInstance:
     return di
 
 
+def row_stride(t) -> int:
+    """Elements between rows; a size-1 leading dim may report any stride."""
+    return int(t.stride(0)) if t.shape[0] > 1 else int(t.shape[1])
+
+
 def _cuda(t, dtype=None):
     t = torch.as_tensor(t)
     if dtype is not None and t.dtype != dtype:
@@ -110,7 +115,7 @@ def makespan_batch(instance, ops, lens, mode: int = N.MODE_EXACT, want_returns: 
     if want_bottleneck and "bottleneck" not in res:
         res["bottleneck"] = torch.empty(Nc, dtype=torch.int32, device=dev)
     L = N.lib()
-    N.check(L.vrp_makespan_batch(di.handle, N.ptr(ops), ops.element_size(), ops.stride(0),
+    N.check(L.vrp_makespan_batch(di.handle, N.ptr(ops), ops.element_size(), row_stride(ops),
                                  N.ptr(lens), Nc, int(mode), N.ptr(res["z"]), N.ptr(res["status"]),
                                  N.ptr(res.get("returns")), N.ptr(res.get("bottleneck")),
                                  N.stream_handle(stream)), "vrp_makespan_batch")
@@ -132,7 +137,7 @@ def evaluate_records(instance, ops, lens, stream=None):
            "arrival": torch.zeros(ops.shape, dtype=torch.float64, device=dev),
            "time": torch.zeros(ops.shape, dtype=torch.float64, device=dev),
            "q0": torch.zeros((Nc, di.m), dtype=torch.int32, device=dev)}
-    N.check(N.lib().vrp_evaluate_records(di.handle, N.ptr(ops), ops.stride(0), N.ptr(lens), Nc,
+    N.check(N.lib().vrp_evaluate_records(di.handle, N.ptr(ops), row_stride(ops), N.ptr(lens), Nc,
                                          N.ptr(res["z"]), N.ptr(res["status"]),
                                          N.ptr(res["returns"]), N.ptr(res["arrival"]),
                                          N.ptr(res["time"]), N.ptr(res["q0"]),
@@ -165,10 +170,10 @@ def decode_batch(instance, genes, relax: bool = True, penalty: float = 1e6,
         res["lens"] = torch.empty((Nc, di.m), dtype=torch.int32, device=dev)
     ops = res.get("ops") if want_solution else None
     N.check(N.lib().vrp_decode_batch(
-        di.handle, N.ptr(genes), genes.stride(0), Nc, int(bool(relax)), float(penalty),
+        di.handle, N.ptr(genes), row_stride(genes), Nc, int(bool(relax)), float(penalty),
         N.ptr(res["fitness"]), N.ptr(res["makespan"]), N.ptr(res["scheduled"]),
         N.ptr(res["visits"]), N.ptr(ops), ops.element_size() if ops is not None else 4,
-        ops.stride(0) if ops is not None else 2 * di.n,
+        row_stride(ops) if ops is not None else 2 * di.n,
         N.ptr(res.get("lens") if want_solution else None), N.stream_handle(stream)),
         "vrp_decode_batch")
     return res
