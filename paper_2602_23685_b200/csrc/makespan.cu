@@ -49,8 +49,8 @@ __host__ __device__ inline WarpLayout warp_layout(int n, bool intd, int mode) {
     WarpLayout L;
     size_t o = 0;
     L.ready = o; o += align16(sizeof(double) * (size_t)(n + 1));
-    L.leg = o;   o += align16((intd ? 4 : 8) * (size_t)(2 * n));
-    L.op = o;    o += align16(sizeof(uint16_t) * (size_t)(2 * n));
+    L.leg = o;   o += align16((intd ? 4 : 8) * (size_t)(2 * n + 2));   // +2: prefetch overrun
+    L.op = o;    o += align16(sizeof(uint16_t) * (size_t)(2 * n + 2));
     L.posd = o;  if (mode == MODE_TWO) o += align16(sizeof(uint16_t) * (size_t)(n + 1));
     L.total = o;
     return L;
@@ -181,12 +181,12 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 for (int i = off; i < end; ++i) {
                     const int op = s_op[i] & 0x7fff;
                     const int c = op_customer(op);
+                    const bool pick = op & 1;
                     t = t + (double)s_leg[i];
-                    if (!(op & 1)) s_ready[c] = t + (double)s_p[c];
-                    else {
-                        const int pd = s_posd[c];
-                        if (pd > i && pd < end) dead = true;
-                    }
+                    const double pc = (double)s_p[c];
+                    const int pd = s_posd[c];
+                    if (!pick) s_ready[c] = t + pc;
+                    dead |= pick && pd > i && pd < end;
                     cap_step(op, k, s, lo, hi);
                 }
             }
@@ -198,43 +198,46 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 for (int i = off; i < end; ++i) {
                     const int op = s_op[i] & 0x7fff;
                     t = t + (double)s_leg[i];
-                    if (op & 1) {
-                        const double r = s_ready[op_customer(op)];
-                        if (r > t) t = r;
-                    }
+                    const double r = s_ready[op_customer(op)];
+                    if ((op & 1) && r > t) t = r;
                 }
             }
         } else {
-            // event replay in rounds; values written by other lanes become
-            // visible at the __syncwarp() closing each round, a lane that reads
-            // an unset ready[c] simply stops and resumes next round
+            // Lockstep dataflow replay: every iteration each lane executes the
+            // next op of its route unless it is a pickup whose dropoff has not
+            // happened yet; writes become visible to the other lanes at the
+            // __syncwarp() ending the iteration, so the iteration count is the
+            // depth of the precedence DAG.  An iteration in which no lane moves
+            // while ops remain is a circular wait.  Branch-free body: both op
+            // kinds are evaluated and the result selected.
             int i = off;
+            int raw0 = s_op[i], raw1 = s_op[i + 1];
+            double leg0 = (double)s_leg[i], leg1 = (double)s_leg[i + 1];
             for (;;) {
-                const int i0 = i;
-                if (vlane) {
-                    while (i < end) {
-                        const int op = s_op[i] & 0x7fff;
-                        const int c = op_customer(op);
-                        const double lg = (double)s_leg[i];
-                        if (!(op & 1)) {
-                            t = t + lg;
-                            s_ready[c] = t + (double)s_p[c];
-                            if (REC) { arrival_out[cand * stride + i] = t; time_out[cand * stride + i] = t; }
-                        } else {
-                            const double r = s_ready[c];
-                            if (r < 0.0) break;  // dropoff not performed yet
-                            const double arr = t + lg;
-                            t = arr >= r ? arr : r;
-                            if (REC) { arrival_out[cand * stride + i] = arr; time_out[cand * stride + i] = t; }
-                        }
-                        cap_step(op, k, s, lo, hi);
-                        ++i;
-                    }
+                const bool active = vlane && i < end;
+                const int op = active ? (raw0 & 0x7fff) : 0;  // past the end: stale slot
+                const int c = op_customer(op);
+                const bool pick = op & 1;
+                const double r = s_ready[c];
+                const double pc = (double)s_p[c];
+                const bool go = active && !(pick && r < 0.0);
+                const double arr = t + leg0;
+                const double tn = (pick && !(arr >= r)) ? r : arr;
+                if (go) {
+                    if (!pick) s_ready[c] = tn + pc;
+                    if (REC) { arrival_out[cand * stride + i] = arr; time_out[cand * stride + i] = tn; }
+                    t = tn;
+                    cap_step(op, k, s, lo, hi);
+                    ++i;
+                    raw0 = raw1; leg0 = leg1;
+                    raw1 = s_op[i + 1];
+                    leg1 = (double)s_leg[i + 1];
                 }
-                const bool prog = i != i0;
+                const unsigned moved = __ballot_sync(VRP_FULL_MASK, go);
+                const unsigned left = __ballot_sync(VRP_FULL_MASK, vlane && i < end);
                 __syncwarp();
-                if (__all_sync(VRP_FULL_MASK, i >= end)) break;
-                if (!__any_sync(VRP_FULL_MASK, prog)) { dead = true; break; }
+                if (!left) break;
+                if (!moved) { dead = true; break; }
             }
             if (dead && vlane)  // finish the capacity test past the stuck position
                 for (int j = i; j < end; ++j) cap_step(s_op[j] & 0x7fff, k, s, lo, hi);
