@@ -1,265 +1,312 @@
 // makespan.cu -- K1 (exact event-driven makespan, schedule.py:188-316) and
 // K2 (two-pass estimate, schedule.py:345-393) over batches of candidates.
 //
-// One warp per candidate, persistent grid (148 SMs x resident blocks).
+// Mapping: a warp carries G = floor(32/m) candidates at once, lane g*m+v owns
+// route v of candidate g (30 of 32 lanes busy for m = 6); persistent grid.
 //
-//  stage   all 32 lanes: stream the candidate's ops into shared memory
-//          (coalesced, evict-first), validate (range / duplicates / count),
-//          and gather every leg d[prev][c] from the L2-resident matrix into
-//          shared memory -- the gathers do not depend on any time value, so
-//          they are issued with full memory-level parallelism;
-//  walk    lane v = vehicle v replays its route from shared memory:
-//          dropoff  t += leg,  ready[c] = t + p[c]
-//          pickup   t = max(t + leg, ready[c])   (blocked while ready[c] unset)
-//          Lanes advance in rounds; a round in which no lane advances while
-//          ops remain is a circular wait (Deadlock, schedule.py:243-245/308-309).
-//          Every value depends only on its DAG predecessors, computed with the
-//          reference's operation order, so the result is bit-identical to the
-//          reference's round-robin replay whatever the interleaving.
-//  reduce  returns = t + d[last][0] (0 for an empty route), z = max, bottleneck
-//          = first argmax, status precedence MALFORMED > CAPACITY > DEADLOCK.
+// Each lane streams its own route through a register pipeline -- op codes
+// loaded OPS_AHEAD positions ahead (read-only path, L1 line reuse), legs
+// d[prev][c] gathered from the L2-resident matrix LEGS_AHEAD positions ahead --
+// so the only shared memory a candidate needs is its ready table
+// ready[c] = t_drop[c] + p[c] (fp64, n+1 slots) plus one block-shared copy of
+// p.  That keeps ~25 candidates in flight per SM at n = 999.
 //
-// The capacity test (route_initial_load, schedule.py:159-185) is the running
-// interval [lo, hi] of feasible initial loads; lo only grows and hi only
-// shrinks, so "empty at some prefix" == "empty at the end" and the test is
-// fused into the walk (finished past a deadlock by a capacity-only scan).
+// Replay (exact / evaluate): lockstep dataflow.  Every iteration each lane
+// executes the next op of its route unless it is a pickup whose dropoff has
+// not happened yet (ready < 0):
+//     dropoff  t = t + leg;                 ready[c] = t + p[c]
+//     pickup   arr = t + leg;  t = arr >= ready[c] ? arr : ready[c]
+// Writes become visible to the other lanes at the __syncwarp() closing the
+// iteration, so the iteration count is the depth of the precedence DAG.  A
+// candidate whose lanes all stall while ops remain is a circular wait
+// (Deadlock, schedule.py:243-245 / :308-309).  Each value depends only on its
+// DAG predecessors and is computed with the reference's fp64 operation order,
+// so results are bit-identical to the reference's round-robin replay.
+//
+// Capacity (route_initial_load, schedule.py:159-185) is the running interval
+// [lo, hi] of feasible initial loads; lo only grows and hi only shrinks, so
+// "empty at some prefix" == "empty at the end" and the test rides along with
+// the replay (finished past a deadlock by a capacity-only scan).  Status
+// precedence: MALFORMED > CAPACITY > DEADLOCK.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace {
 
 constexpr int MODE_EXACT = 0, MODE_EVAL = 1, MODE_TWO = 2;
-constexpr uint16_t START_BIT = 0x8000;  // marks the first op of a route in s_op
 constexpr int ST_OK = 0, ST_CAP = 1, ST_DEAD = 2, ST_MAL = 3;
-constexpr int GATHER_BATCH = 16;         // independent L2 gathers in flight per lane
+constexpr int OPS_AHEAD = 8;   // op codes in registers (positions i .. i+7)
+constexpr int LEGS_AHEAD = 4;  // gathered legs in registers (positions i .. i+3)
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-template <bool INTD>
-struct LegType { using T = double; };
-template <>
-struct LegType<true> { using T = int32_t; };
-
-// Per-warp shared-memory slots (one candidate in flight per warp) ...
-struct WarpLayout {
-    size_t ready, leg, op, posd, total;
+// Per candidate: ready table, plus (validating modes) an op bitmap and (two-
+// pass) the (route, position) of every dropoff.
+struct CandLayout {
+    size_t ready, bits, posd, total;
 };
 
-__host__ __device__ inline WarpLayout warp_layout(int n, bool intd, int mode) {
-    WarpLayout L;
+__host__ __device__ inline CandLayout cand_layout(int n, int mode) {
+    CandLayout L;
     size_t o = 0;
     L.ready = o; o += align16(sizeof(double) * (size_t)(n + 1));
-    L.leg = o;   o += align16((intd ? 4 : 8) * (size_t)(2 * n + 2));   // +2: prefetch overrun
-    L.op = o;    o += align16(sizeof(uint16_t) * (size_t)(2 * n + 2));
-    L.posd = o;  if (mode == MODE_TWO) o += align16(sizeof(uint16_t) * (size_t)(n + 1));
+    L.bits = o;  if (mode != MODE_EXACT) o += align16(sizeof(uint32_t) * (size_t)((2 * n + 31) / 32));
+    L.posd = o;  if (mode == MODE_TWO) o += align16(sizeof(uint32_t) * (size_t)(n + 1));
     L.total = o;
     return L;
 }
 
-// ... plus one block-shared copy of p (processing times), read on every dropoff.
-__host__ __device__ inline size_t block_p_bytes(int n, bool intd) {
-    return align16((intd ? 4 : 8) * (size_t)(n + 1));
-}
+__host__ __device__ inline size_t block_p_bytes(int n) { return align16(sizeof(double) * (size_t)(n + 1)); }
 
 __device__ __forceinline__ void cap_step(int op, int k, int &s, int &lo, int &hi) {
     if (op & 1) { int room = k - 1 - s; hi = room < hi ? room : hi; ++s; }
     else        { int need = 1 - s;     lo = need > lo ? need : lo; --s; }
 }
 
+// One route's op codes and legs, streamed through registers.  Positions past
+// the end read as -1; out-of-range codes are reported through `bad` and
+// replaced by op 0 so that no gather leaves the matrix.
+template <typename OpT, bool INTD>
+struct RouteStream {
+    const OpT *rp;
+    int L, i, two_n;
+    int o[OPS_AHEAD];
+    double l[LEGS_AHEAD];
+    bool bad;
+
+    __device__ __forceinline__ int fetch(int pos) {
+        if (pos >= L) return -1;
+        int op = (int)__ldg(rp + pos);
+        if (op < 0 || op >= two_n) { bad = true; op = 0; }
+        return op;
+    }
+    __device__ __forceinline__ double leg(const DevInstance &I, int prev_op, int op) const {
+        if (op < 0) return 0.0;
+        const int a = prev_op < 0 ? 0 : op_customer(prev_op);
+        return dist<INTD>(I, a, op_customer(op));
+    }
+    __device__ __forceinline__ void init(const DevInstance &I, const OpT *route, int len, int n2) {
+        rp = route; L = len; i = 0; two_n = n2; bad = false;
+#pragma unroll
+        for (int q = 0; q < OPS_AHEAD; ++q) o[q] = fetch(q);
+        l[0] = leg(I, -1, o[0]);
+#pragma unroll
+        for (int q = 1; q < LEGS_AHEAD; ++q) l[q] = leg(I, o[q - 1], o[q]);
+    }
+    __device__ __forceinline__ void advance(const DevInstance &I) {
+        ++i;
+#pragma unroll
+        for (int q = 0; q + 1 < OPS_AHEAD; ++q) o[q] = o[q + 1];
+        o[OPS_AHEAD - 1] = fetch(i + OPS_AHEAD - 1);
+#pragma unroll
+        for (int q = 0; q + 1 < LEGS_AHEAD; ++q) l[q] = l[q + 1];
+        l[LEGS_AHEAD - 1] = leg(I, o[LEGS_AHEAD - 2], o[LEGS_AHEAD - 1]);
+    }
+};
+
 template <typename OpT, bool INTD, int MODE, bool REC>
 __global__ void __launch_bounds__(256)
 makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
-                const int32_t *__restrict__ lens, int64_t N, double *__restrict__ z_out,
+                const int32_t *__restrict__ lens, int64_t N, int G, double *__restrict__ z_out,
                 int32_t *__restrict__ status_out, double *__restrict__ returns_out,
                 int32_t *__restrict__ bottleneck_out, double *__restrict__ arrival_out,
                 double *__restrict__ time_out, int32_t *__restrict__ q0_out) {
-    using LegT = typename LegType<INTD>::T;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int n = I.n, m = I.m, k = I.k, two_n = 2 * n;
-    const WarpLayout Lw = warp_layout(n, INTD, MODE);
-    LegT *s_p = reinterpret_cast<LegT *>(smem);
-    unsigned char *base = smem + block_p_bytes(n, INTD) + (size_t)warp * Lw.total;
-    double *s_ready = reinterpret_cast<double *>(base + Lw.ready);
-    uint32_t *s_bits = reinterpret_cast<uint32_t *>(base + Lw.ready);  // validation bitmap (aliases ready)
-    LegT *s_leg = reinterpret_cast<LegT *>(base + Lw.leg);
-    uint16_t *s_op = reinterpret_cast<uint16_t *>(base + Lw.op);
-    uint16_t *s_posd = reinterpret_cast<uint16_t *>(base + Lw.posd);
-    const bool vlane = lane < m;
+    const CandLayout CL = cand_layout(n, MODE);
+    double *s_p = reinterpret_cast<double *>(smem);
+    unsigned char *wbase = smem + block_p_bytes(n) + (size_t)warp * G * CL.total;
 
-    for (int c = threadIdx.x; c <= n; c += blockDim.x)
-        s_p[c] = INTD ? (LegT)__ldg(I.p32 + c) : (LegT)__ldg(I.p + c);
+    const int g = lane / m, v = lane - (lane / m) * m;
+    const bool glane = g < G;
+    const unsigned gmask = glane ? (((m == 32) ? 0xffffffffu : ((1u << m) - 1u)) << (g * m)) : 0u;
+    const int leader = g * m;  // lane holding route 0 of this lane's candidate
+    unsigned char *cbase = wbase + (size_t)(glane ? g : 0) * CL.total;
+    double *s_ready = reinterpret_cast<double *>(cbase + CL.ready);
+    uint32_t *s_posd = reinterpret_cast<uint32_t *>(cbase + CL.posd);
+
+    for (int c = threadIdx.x; c <= n; c += blockDim.x) s_p[c] = __ldg(I.p + c);
     __syncthreads();
 
-    for (int64_t cand = (int64_t)blockIdx.x * wpb + warp; cand < N;
-         cand += (int64_t)gridDim.x * wpb) {
-        const OpT *row = ops + cand * stride;
-        // ---- route offsets (lane v owns route v)
-        int L = vlane ? __ldg(lens + cand * m + lane) : 0;
-        int off = L;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int y = __shfl_up_sync(VRP_FULL_MASK, off, o);
-            if (lane >= o) off += y;
+    const int64_t step = (int64_t)gridDim.x * wpb * G;
+    for (int64_t base = ((int64_t)blockIdx.x * wpb + warp) * G; base < N; base += step) {
+        const int64_t cand = base + g;
+        const bool live = glane && cand < N;
+        // ---- route offsets: lane v sums the lengths of routes 0..v-1
+        int L = 0, off = 0, total = 0;
+        bool mal = false;
+        if (live) {
+            const int32_t *lr = lens + cand * m;
+            for (int u = 0; u < m; ++u) {
+                const int x = __ldg(lr + u);
+                mal |= x < 0;
+                if (u < v) off += x;
+                if (u == v) L = x;
+                total += x;
+            }
+            mal |= total > two_n || total > stride || (MODE != MODE_EXACT && total != two_n);
         }
-        const int total = __shfl_sync(VRP_FULL_MASK, off, 31);
-        off -= L;  // exclusive
-        bool bad = __any_sync(VRP_FULL_MASK, L < 0) || total > two_n ||
-                   (MODE != MODE_EXACT && total != two_n) || total > stride;
+        const OpT *row = ops + (live ? cand : 0) * stride;
 
-        // ---- stage ops (streaming loads) + validation
-        if (MODE != MODE_EXACT && !bad) {
-            for (int w = lane; w < (two_n + 31) / 32; w += 32) s_bits[w] = 0u;
-            __syncwarp();
+        // ---- shared tables: ready = -1 (dropoff not done); validation bitmap
+        for (int gg = 0; gg < G; ++gg) {
+            double *rd = reinterpret_cast<double *>(wbase + (size_t)gg * CL.total + CL.ready);
+            for (int c = lane; c <= n; c += 32) rd[c] = -1.0;
+            if (MODE != MODE_EXACT) {
+                uint32_t *bt = reinterpret_cast<uint32_t *>(wbase + (size_t)gg * CL.total + CL.bits);
+                for (int w = lane; w < (two_n + 31) / 32; w += 32) bt[w] = 0u;
+            }
         }
-        if (!bad) {
-            bool mine_bad = false;
-#pragma unroll 4
-            for (int j = lane; j < total; j += 32) {
-                int op = (int)load_stream(row + j);
-                if (op < 0 || op >= two_n) { mine_bad = true; op = 0; }
-                s_op[j] = (uint16_t)op;
-                if (MODE != MODE_EXACT) {
-                    uint32_t bit = 1u << (op & 31);
-                    uint32_t prev = atomicOr(&s_bits[op >> 5], bit);
-                    if (prev & bit) mine_bad = true;
+        __syncwarp();
+        if (MODE != MODE_EXACT) {
+            // duplicates / range (schedule.py:134-156): the whole warp streams
+            // each candidate's ops, coalesced
+            for (int gg = 0; gg < G; ++gg) {
+                const int64_t cg = base + gg;
+                const int tg = __shfl_sync(VRP_FULL_MASK, total, gg * m);
+                const int mg = __shfl_sync(VRP_FULL_MASK, (int)mal, gg * m);
+                if (cg >= N || mg) continue;
+                uint32_t *bt = reinterpret_cast<uint32_t *>(wbase + (size_t)gg * CL.total + CL.bits);
+                bool dup = false;
+                for (int j = lane; j < tg; j += 32) {
+                    const int op = (int)__ldg(ops + cg * stride + j);
+                    if (op < 0 || op >= two_n) { dup = true; continue; }
+                    const uint32_t bit = 1u << (op & 31);
+                    dup |= (atomicOr(&bt[op >> 5], bit) & bit) != 0;
                 }
+                const bool anyd = __any_sync(VRP_FULL_MASK, dup);
+                if (glane && g == gg) mal |= anyd;
             }
-            bad = __any_sync(VRP_FULL_MASK, mine_bad);
         }
-        if (bad) {
-            if (lane == 0) {
-                z_out[cand] = 0.0;
-                status_out[cand] = ST_MAL;
-                if (bottleneck_out) bottleneck_out[cand] = 0;
-            }
-            if (returns_out && vlane) returns_out[cand * m + lane] = 0.0;
-            __syncwarp();
-            continue;
-        }
-        __syncwarp();
-        if (vlane && L > 0) s_op[off] |= START_BIT;
-        __syncwarp();
+        mal = (__ballot_sync(VRP_FULL_MASK, live && mal) & gmask) != 0;
+        const bool run = live && !mal;
 
-        // ---- gather legs d[prev][c]: independent of all times, so issue
-        // GATHER_BATCH loads per lane before consuming any of them
-        for (int j0 = lane; j0 < total; j0 += 32 * GATHER_BATCH) {
-            int64_t addr[GATHER_BATCH];
-#pragma unroll
-            for (int u = 0; u < GATHER_BATCH; ++u) {
-                const int j = j0 + 32 * u;
-                addr[u] = 0;
-                if (j < total) {
-                    const int raw = s_op[j];
-                    const int c = op_customer(raw & 0x7fff);
-                    const int prev = (raw & START_BIT) ? 0 : op_customer(s_op[j - 1] & 0x7fff);
-                    addr[u] = (int64_t)prev * I.W + c;
-                    if (MODE == MODE_TWO && !(raw & 1)) s_posd[c] = (uint16_t)j;
-                }
-            }
-            LegT v[GATHER_BATCH];
-#pragma unroll
-            for (int u = 0; u < GATHER_BATCH; ++u)
-                v[u] = INTD ? (LegT)__ldg(I.d32 + addr[u]) : (LegT)__ldg(I.d + addr[u]);
-#pragma unroll
-            for (int u = 0; u < GATHER_BATCH; ++u)
-                if (j0 + 32 * u < total) s_leg[j0 + 32 * u] = v[u];
-        }
-        for (int c = lane; c <= n; c += 32) s_ready[c] = -1.0;  // -1: dropoff not done
-        __syncwarp();
-
-        const int end = off + L;
+        RouteStream<OpT, INTD> rs;
+        rs.init(I, row + off, run ? L : 0, two_n);
         double t = 0.0;
-        int s = 0, lo = 0, hi = k;
-        bool dead = false;
+        int s = 0, lo = 0, hi = k, lastc = 0;
+        bool dead = false, bad_ops = false;
+
         if (MODE == MODE_TWO) {
-            // pass 1: no-wait walk, ready = dropoff time + p (schedule.py:371-378);
-            // same-route pickup before its own dropoff => Deadlock (:362-369)
-            if (vlane) {
-                for (int i = off; i < end; ++i) {
-                    const int op = s_op[i] & 0x7fff;
-                    const int c = op_customer(op);
-                    const bool pick = op & 1;
-                    t = t + (double)s_leg[i];
-                    const double pc = (double)s_p[c];
-                    const int pd = s_posd[c];
-                    if (!pick) s_ready[c] = t + pc;
-                    dead |= pick && pd > i && pd < end;
-                    cap_step(op, k, s, lo, hi);
+            // pass 1: no-wait walk; ready = dropoff time + p (schedule.py:371-378)
+            while (rs.i < rs.L) {
+                const int op = rs.o[0];
+                const int c = op_customer(op);
+                t = t + rs.l[0];
+                if (!(op & 1)) {
+                    s_ready[c] = t + s_p[c];
+                    s_posd[c] = ((uint32_t)v << 16) | (uint32_t)rs.i;
                 }
+                cap_step(op, k, s, lo, hi);
+                lastc = c;
+                rs.advance(I);
             }
-            dead = __any_sync(VRP_FULL_MASK, dead);
+            bad_ops = rs.bad;
             __syncwarp();
-            // pass 2: waits at pickups (schedule.py:380-393)
+            // pass 2: waits at pickups (schedule.py:380-393), and the same-route
+            // pickup-before-its-dropoff Deadlock (:362-369)
+            rs.init(I, row + off, run ? L : 0, two_n);
             t = 0.0;
-            if (vlane && !dead) {
-                for (int i = off; i < end; ++i) {
-                    const int op = s_op[i] & 0x7fff;
-                    t = t + (double)s_leg[i];
-                    const double r = s_ready[op_customer(op)];
-                    if ((op & 1) && r > t) t = r;
+            while (rs.i < rs.L) {
+                const int op = rs.o[0];
+                const int c = op_customer(op);
+                t = t + rs.l[0];
+                if (op & 1) {
+                    const double r = s_ready[c];
+                    if (r > t) t = r;
+                    const uint32_t pd = s_posd[c];
+                    dead |= (int)(pd >> 16) == v && (int)(pd & 0xffffu) > rs.i;
                 }
+                rs.advance(I);
             }
         } else {
-            // Lockstep dataflow replay: every iteration each lane executes the
-            // next op of its route unless it is a pickup whose dropoff has not
-            // happened yet; writes become visible to the other lanes at the
-            // __syncwarp() ending the iteration, so the iteration count is the
-            // depth of the precedence DAG.  An iteration in which no lane moves
-            // while ops remain is a circular wait.  Branch-free body: both op
-            // kinds are evaluated and the result selected.
-            int i = off;
-            int raw0 = s_op[i], raw1 = s_op[i + 1];
-            double leg0 = (double)s_leg[i], leg1 = (double)s_leg[i + 1];
             for (;;) {
-                const bool active = vlane && i < end;
-                const int op = active ? (raw0 & 0x7fff) : 0;  // past the end: stale slot
+                const bool active = run && !dead && rs.i < rs.L;
+                const int op = active ? rs.o[0] : 0;
                 const int c = op_customer(op);
                 const bool pick = op & 1;
                 const double r = s_ready[c];
-                const double pc = (double)s_p[c];
+                const double pc = s_p[c];
                 const bool go = active && !(pick && r < 0.0);
-                const double arr = t + leg0;
+                const double arr = t + rs.l[0];
                 const double tn = (pick && !(arr >= r)) ? r : arr;
                 if (go) {
                     if (!pick) s_ready[c] = tn + pc;
-                    if (REC) { arrival_out[cand * stride + i] = arr; time_out[cand * stride + i] = tn; }
+                    if (REC) {
+                        const int64_t at = cand * stride + off + rs.i;
+                        arrival_out[at] = arr;
+                        time_out[at] = tn;
+                    }
                     t = tn;
+                    lastc = c;
                     cap_step(op, k, s, lo, hi);
-                    ++i;
-                    raw0 = raw1; leg0 = leg1;
-                    raw1 = s_op[i + 1];
-                    leg1 = (double)s_leg[i + 1];
+                    rs.advance(I);
                 }
                 const unsigned moved = __ballot_sync(VRP_FULL_MASK, go);
-                const unsigned left = __ballot_sync(VRP_FULL_MASK, vlane && i < end);
+                const unsigned left = __ballot_sync(VRP_FULL_MASK, active && rs.i < rs.L);
                 __syncwarp();
                 if (!left) break;
-                if (!moved) { dead = true; break; }
+                if ((left & gmask) && !(moved & gmask)) dead = true;  // this candidate is stuck
             }
-            if (dead && vlane)  // finish the capacity test past the stuck position
-                for (int j = i; j < end; ++j) cap_step(s_op[j] & 0x7fff, k, s, lo, hi);
+            if (dead)  // finish the capacity test past the stuck position
+                for (int j = rs.i; j < rs.L; ++j) cap_step(rs.fetch(j), k, s, lo, hi);
+            bad_ops = rs.bad;
         }
-        const bool capfail = __any_sync(VRP_FULL_MASK, vlane && lo > hi);
-        const int st = capfail ? ST_CAP : (dead ? ST_DEAD : ST_OK);
+        mal = mal || ((__ballot_sync(VRP_FULL_MASK, live && bad_ops) & gmask) != 0);
+        const bool capfail = (__ballot_sync(VRP_FULL_MASK, live && lo > hi) & gmask) != 0;
+        const bool gdead = (__ballot_sync(VRP_FULL_MASK, live && dead) & gmask) != 0;
+        const int st = mal ? ST_MAL : (capfail ? ST_CAP : (gdead ? ST_DEAD : ST_OK));
 
         double ret = 0.0;
-        if (st == ST_OK && vlane && L > 0)
-            ret = t + dist<INTD>(I, op_customer(s_op[end - 1] & 0x7fff), 0);
-        double z = warp_max(ret);  // returns are >= 0; empty routes count as 0
-        if (st != ST_OK) z = 0.0;
-        const unsigned bmask = __ballot_sync(VRP_FULL_MASK, vlane && ret == z);
-        if (lane == 0) {
-            z_out[cand] = z;
-            status_out[cand] = st;
-            if (bottleneck_out) bottleneck_out[cand] = bmask ? __ffs(bmask) - 1 : 0;
+        if (live && st == ST_OK && L > 0) ret = t + dist<INTD>(I, lastc, 0);
+        double z = 0.0;  // returns are >= 0; empty routes count as 0
+        for (int u = 0; u < m; ++u) {
+            const double x = __shfl_sync(VRP_FULL_MASK, ret, glane ? leader + u : lane);
+            z = x > z ? x : z;
         }
-        if (returns_out && vlane) returns_out[cand * m + lane] = st == ST_OK ? ret : 0.0;
-        if (REC && q0_out && vlane) q0_out[cand * m + lane] = lo;
+        const unsigned bm = __ballot_sync(VRP_FULL_MASK, live && ret == z) & gmask;
+        if (live && v == 0) {
+            z_out[cand] = st == ST_OK ? z : 0.0;
+            status_out[cand] = st;
+            if (bottleneck_out) bottleneck_out[cand] = bm ? __ffs(bm) - 1 - leader : 0;
+        }
+        if (live && returns_out) returns_out[cand * m + v] = st == ST_OK ? ret : 0.0;
+        if (REC && live && q0_out) q0_out[cand * m + v] = lo;
         __syncwarp();
     }
+}
+
+// (candidates per warp, warps per block) maximising resident candidates per SM
+struct Shape {
+    int G, wpb, blocks;
+    size_t smem;
+};
+
+template <typename Kern>
+int plan(Kern kern, int n, int m, int mode, Shape &out) {
+    const size_t per_cand = cand_layout(n, mode).total;
+    const size_t pbytes = block_p_bytes(n);
+    const int gmax = 32 / m;
+    long best = -1;
+    for (int G = gmax; G >= 1; --G) {
+        for (int w = 8; w >= 1; --w) {
+            const size_t bytes = pbytes + (size_t)w * G * per_cand;
+            if (bytes > 227 * 1024) continue;
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+                return -1;
+            int blocks = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32 * w, bytes) != cudaSuccess)
+                return -1;
+            // most resident candidates; among equals, fewer warps (fewer instructions)
+            const long score = (long)blocks * w * G * 64 - (long)blocks * w;
+            if (blocks > 0 && score > best) { best = score; out = {G, w, blocks, bytes}; }
+        }
+    }
+    if (best < 0) return -2;
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)out.smem) == cudaSuccess ? 0 : -1;
 }
 
 template <typename OpT, bool INTD, int MODE, bool REC>
@@ -267,37 +314,21 @@ int launch_t(const DevInstance &I, const void *ops, int64_t stride, const int32_
              int64_t N, double *z, int32_t *status, double *returns, int32_t *bottleneck,
              double *arrival, double *timev, int32_t *q0, cudaStream_t stream, int sm_count) {
     auto kern = makespan_kernel<OpT, INTD, MODE, REC>;
-    const size_t per_warp = warp_layout(I.n, INTD, MODE).total;
-    const size_t shared_p = block_p_bytes(I.n, INTD);
-    // choose warps/block maximising resident warps per SM under the smem
-    // budget; cached per instantiation for the last per-warp footprint
-    static size_t cached_pw = 0;
-    static int cached_w = 0, cached_blocks = 0;
-    int best_w = 1, best_res = 0, best_blocks = 1;
-    const bool hit = cached_pw == per_warp;
-    if (hit) { best_w = cached_w; best_blocks = cached_blocks; best_res = 1; }
-    for (int w = 8; w >= 1 && !hit; --w) {
-        size_t bytes = shared_p + per_warp * (size_t)w;
-        if (bytes > 227 * 1024) continue;
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
-            return -1;
-        int blocks = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32 * w, bytes) != cudaSuccess)
-            return -1;
-        if (blocks * w > best_res) { best_res = blocks * w; best_w = w; best_blocks = blocks; }
+    static int cached_n = -1, cached_m = -1;
+    static Shape sh;
+    if (cached_n != I.n || cached_m != I.m) {
+        const int rc = plan(kern, I.n, I.m, MODE, sh);
+        if (rc) return rc;
+        cached_n = I.n;
+        cached_m = I.m;
     }
-    if (best_res == 0) return -2;
-    size_t bytes = shared_p + per_warp * (size_t)best_w;
-    if (cached_pw != per_warp) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-        cached_pw = per_warp; cached_w = best_w; cached_blocks = best_blocks;
-    }
-    int64_t want = (N + best_w - 1) / best_w;
-    int64_t grid = (int64_t)best_blocks * sm_count;
+    const int64_t per_block = (int64_t)sh.wpb * sh.G;
+    const int64_t want = (N + per_block - 1) / per_block;
+    int64_t grid = (int64_t)sh.blocks * sm_count;
     if (grid > want) grid = want;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, 32 * best_w, bytes, stream>>>(
-        I, static_cast<const OpT *>(ops), stride, lens, N, z, status, returns, bottleneck,
+    kern<<<(unsigned)grid, 32 * sh.wpb, sh.smem, stream>>>(
+        I, static_cast<const OpT *>(ops), stride, lens, N, sh.G, z, status, returns, bottleneck,
         arrival, timev, q0);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
 }
