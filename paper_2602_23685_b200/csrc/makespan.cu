@@ -63,32 +63,52 @@ __device__ __forceinline__ void cap_step(int op, int k, int &s, int &lo, int &hi
     else        { int need = 1 - s;     lo = need > lo ? need : lo; --s; }
 }
 
-// One route's op codes and legs, streamed through registers.  Positions past
-// the end read as -1; out-of-range codes are reported through `bad` and
+// One route's op codes and legs, streamed through registers.  Loads enter at
+// the back of the pipeline and are only consumed stages later, so neither the
+// op load (L1) nor the leg gather (L2) sits on the per-iteration critical
+// path: an op code is range-checked when it reaches the gather stage
+// (LEGS_AHEAD-1), a gathered leg is converted to fp64 when it reaches stage 0.
+// Positions past the end read as -1; out-of-range codes set `bad` and are
 // replaced by op 0 so that no gather leaves the matrix.
+template <bool INTD>
+struct LegRaw { using T = double; };
+template <>
+struct LegRaw<true> { using T = int32_t; };
+
+template <bool INTD>
+__device__ __forceinline__ typename LegRaw<INTD>::T gather_leg(const DevInstance &I, int a, int b) {
+    // L2-only load: the random d gathers must not evict the op-stream lines from L1
+    if (INTD) return (typename LegRaw<INTD>::T)__ldcg(I.d32 + (int64_t)a * I.W + b);
+    return (typename LegRaw<INTD>::T)__ldcg(I.d + (int64_t)a * I.W + b);
+}
+
 template <typename OpT, bool INTD>
 struct RouteStream {
+    using LT = typename LegRaw<INTD>::T;
     const OpT *rp;
     int L, i, two_n;
     int o[OPS_AHEAD];
-    double l[LEGS_AHEAD];
+    LT l[LEGS_AHEAD];
     bool bad;
 
-    __device__ __forceinline__ int fetch(int pos) {
+    __device__ __forceinline__ int fetch(int pos) const { return pos < L ? (int)__ldg(rp + pos) : -1; }
+    // validate the op at route position `pos` (past the end -> -1 sentinel)
+    __device__ __forceinline__ int checked(int op, int pos) {
         if (pos >= L) return -1;
-        int op = (int)__ldg(rp + pos);
-        if (op < 0 || op >= two_n) { bad = true; op = 0; }
+        if ((unsigned)op >= (unsigned)two_n) { bad = true; return 0; }
         return op;
     }
-    __device__ __forceinline__ double leg(const DevInstance &I, int prev_op, int op) const {
-        if (op < 0) return 0.0;
-        const int a = prev_op < 0 ? 0 : op_customer(prev_op);
-        return dist<INTD>(I, a, op_customer(op));
+    __device__ __forceinline__ LT leg(const DevInstance &I, int prev_op, int op) const {
+        if (op < 0) return (LT)0;
+        return gather_leg<INTD>(I, prev_op < 0 ? 0 : op_customer(prev_op), op_customer(op));
     }
+    __device__ __forceinline__ double leg0() const { return (double)l[0]; }
     __device__ __forceinline__ void init(const DevInstance &I, const OpT *route, int len, int n2) {
         rp = route; L = len; i = 0; two_n = n2; bad = false;
 #pragma unroll
         for (int q = 0; q < OPS_AHEAD; ++q) o[q] = fetch(q);
+#pragma unroll
+        for (int q = 0; q < LEGS_AHEAD; ++q) o[q] = checked(o[q], q);
         l[0] = leg(I, -1, o[0]);
 #pragma unroll
         for (int q = 1; q < LEGS_AHEAD; ++q) l[q] = leg(I, o[q - 1], o[q]);
@@ -98,10 +118,13 @@ struct RouteStream {
 #pragma unroll
         for (int q = 0; q + 1 < OPS_AHEAD; ++q) o[q] = o[q + 1];
         o[OPS_AHEAD - 1] = fetch(i + OPS_AHEAD - 1);
+        o[LEGS_AHEAD - 1] = checked(o[LEGS_AHEAD - 1], i + LEGS_AHEAD - 1);
 #pragma unroll
         for (int q = 0; q + 1 < LEGS_AHEAD; ++q) l[q] = l[q + 1];
         l[LEGS_AHEAD - 1] = leg(I, o[LEGS_AHEAD - 2], o[LEGS_AHEAD - 1]);
     }
+    // re-read and validate the op at `pos` (capacity scan past a deadlock)
+    __device__ __forceinline__ int checked_at(int pos) { return checked(fetch(pos), pos); }
 };
 
 template <typename OpT, bool INTD, int MODE, bool REC>
@@ -195,7 +218,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             while (rs.i < rs.L) {
                 const int op = rs.o[0];
                 const int c = op_customer(op);
-                t = t + rs.l[0];
+                t = t + rs.leg0();
                 if (!(op & 1)) {
                     s_ready[c] = t + s_p[c];
                     s_posd[c] = ((uint32_t)v << 16) | (uint32_t)rs.i;
@@ -213,7 +236,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             while (rs.i < rs.L) {
                 const int op = rs.o[0];
                 const int c = op_customer(op);
-                t = t + rs.l[0];
+                t = t + rs.leg0();
                 if (op & 1) {
                     const double r = s_ready[c];
                     if (r > t) t = r;
@@ -231,7 +254,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 const double r = s_ready[c];
                 const double pc = s_p[c];
                 const bool go = active && !(pick && r < 0.0);
-                const double arr = t + rs.l[0];
+                const double arr = t + rs.leg0();
                 const double tn = (pick && !(arr >= r)) ? r : arr;
                 if (go) {
                     if (!pick) s_ready[c] = tn + pc;
@@ -252,7 +275,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 if ((left & gmask) && !(moved & gmask)) dead = true;  // this candidate is stuck
             }
             if (dead)  // finish the capacity test past the stuck position
-                for (int j = rs.i; j < rs.L; ++j) cap_step(rs.fetch(j), k, s, lo, hi);
+                for (int j = rs.i; j < rs.L; ++j) cap_step(rs.checked_at(j), k, s, lo, hi);
             bad_ops = rs.bad;
         }
         mal = mal || ((__ballot_sync(VRP_FULL_MASK, live && bad_ops) & gmask) != 0);
