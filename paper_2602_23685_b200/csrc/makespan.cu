@@ -4,12 +4,11 @@
 // Mapping: a warp carries G = floor(32/m) candidates at once, lane g*m+v owns
 // route v of candidate g (30 of 32 lanes busy for m = 6); persistent grid.
 //
-// Each lane streams its own route through a register pipeline -- op codes
-// loaded OPS_AHEAD positions ahead (read-only path, L1 line reuse), legs
-// d[prev][c] gathered from the L2-resident matrix LEGS_AHEAD positions ahead --
-// so the only shared memory a candidate needs is its ready table
-// ready[c] = t_drop[c] + p[c] (fp64, n+1 slots) plus one block-shared copy of
-// p.  That keeps ~25 candidates in flight per SM at n = 999.
+// Each lane streams its own route through a small cp.async ring (op words
+// fetched ahead, legs d[prev][c] gathered ahead from the L2-resident matrix;
+// see RouteStream), so the only large shared-memory object per candidate is
+// its ready table ready[c] = t_drop[c] + p[c] (fp64, n+1 slots), plus one
+// block-shared copy of p.  That keeps 25 candidates in flight per SM at n=999.
 //
 // Replay (exact / evaluate): lockstep dataflow.  Every iteration each lane
 // executes the next op of its route unless it is a pickup whose dropoff has
@@ -28,6 +27,8 @@
 // "empty at some prefix" == "empty at the end" and the test rides along with
 // the replay (finished past a deadlock by a capacity-only scan).  Status
 // precedence: MALFORMED > CAPACITY > DEADLOCK.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -35,8 +36,6 @@ namespace {
 
 constexpr int MODE_EXACT = 0, MODE_EVAL = 1, MODE_TWO = 2;
 constexpr int ST_OK = 0, ST_CAP = 1, ST_DEAD = 2, ST_MAL = 3;
-constexpr int OPS_AHEAD = 8;   // op codes in registers (positions i .. i+7)
-constexpr int LEGS_AHEAD = 4;  // gathered legs in registers (positions i .. i+3)
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -63,68 +62,98 @@ __device__ __forceinline__ void cap_step(int op, int k, int &s, int &lo, int &hi
     else        { int need = 1 - s;     lo = need > lo ? need : lo; --s; }
 }
 
-// One route's op codes and legs, streamed through registers.  Loads enter at
-// the back of the pipeline and are only consumed stages later, so neither the
-// op load (L1) nor the leg gather (L2) sits on the per-iteration critical
-// path: an op code is range-checked when it reaches the gather stage
-// (LEGS_AHEAD-1), a gathered leg is converted to fp64 when it reaches stage 0.
-// Positions past the end read as -1; out-of-range codes set `bad` and are
-// replaced by op 0 so that no gather leaves the matrix.
-template <bool INTD>
-struct LegRaw { using T = double; };
-template <>
-struct LegRaw<true> { using T = int32_t; };
+// One route's op codes and legs, streamed through a per-lane shared-memory
+// ring filled by cp.async (LDGSTS): op words (4 B = 2 int16 or 1 int32 op
+// codes) are issued OP_WORDS words ahead, legs d[prev][c] are gathered
+// LEG_AHEAD positions ahead into LEG_SLOTS slots.  Every advance commits one
+// async group; consuming position i first waits until at most LEG_AHEAD-1
+// groups are pending, which covers the leg of position i (committed LEG_AHEAD-1
+// advances ago) and every op word that can be read (OP_WORDS >= 2*LEG_AHEAD).
+// No register ever waits on an in-flight load, so the walk's per-iteration
+// latency is only its own dependency chain.  Out-of-range op codes set `bad`
+// and read as op 0 so that no gather leaves the matrix.
+constexpr int LEG_AHEAD = 6;
+constexpr int LEG_SLOTS = 8;   // power of two >= LEG_AHEAD
+constexpr int OP_WORDS = 16;   // power of two >= 2 * LEG_AHEAD
 
-template <bool INTD>
-__device__ __forceinline__ typename LegRaw<INTD>::T gather_leg(const DevInstance &I, int a, int b) {
-    // L2-only load: the random d gathers must not evict the op-stream lines from L1
-    if (INTD) return (typename LegRaw<INTD>::T)__ldcg(I.d32 + (int64_t)a * I.W + b);
-    return (typename LegRaw<INTD>::T)__ldcg(I.d + (int64_t)a * I.W + b);
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__host__ __device__ constexpr size_t ring_bytes(bool intd) {
+    return (size_t)OP_WORDS * 4 + (size_t)LEG_SLOTS * (intd ? 4 : 8);
 }
 
 template <typename OpT, bool INTD>
 struct RouteStream {
-    using LT = typename LegRaw<INTD>::T;
-    const OpT *rp;
+    using LT = typename std::conditional<INTD, int32_t, double>::type;
+    static constexpr int E = sizeof(OpT) == 2 ? 2 : 1;  // op codes per 4-byte word
+    const uint32_t *words;  // ops buffer viewed as 4-byte words
+    int64_t ge0;            // element index of route position 0
     int L, i, two_n;
-    int o[OPS_AHEAD];
-    LT l[LEGS_AHEAD];
+    int64_t next_w, last_w; // next word to issue, last word of the route
+    uint32_t *rw;           // ring: op words
+    LT *rl;                 // ring: legs
     bool bad;
 
-    __device__ __forceinline__ int fetch(int pos) const { return pos < L ? (int)__ldg(rp + pos) : -1; }
-    // validate the op at route position `pos` (past the end -> -1 sentinel)
-    __device__ __forceinline__ int checked(int op, int pos) {
+    __device__ __forceinline__ int64_t word_of(int pos) const { return (ge0 + pos) / E; }
+    __device__ __forceinline__ void issue_word() {
+        cp_async4(rw + (next_w & (OP_WORDS - 1)), words + next_w);
+        ++next_w;
+    }
+    // op code at route position pos (its word must have landed); -1 past the end
+    __device__ __forceinline__ int op_at(int pos) const {
         if (pos >= L) return -1;
-        if ((unsigned)op >= (unsigned)two_n) { bad = true; return 0; }
-        return op;
+        const int64_t ge = ge0 + pos;
+        const uint32_t w = rw[(ge / E) & (OP_WORDS - 1)];
+        if (E == 2) return (int)(int16_t)(w >> ((ge & 1) * 16));
+        return (int)w;
     }
-    __device__ __forceinline__ LT leg(const DevInstance &I, int prev_op, int op) const {
-        if (op < 0) return (LT)0;
-        return gather_leg<INTD>(I, prev_op < 0 ? 0 : op_customer(prev_op), op_customer(op));
+    __device__ __forceinline__ int safe(int op) const { return (unsigned)op < (unsigned)two_n ? op : 0; }
+    __device__ __forceinline__ void issue_leg(const DevInstance &I, int pos) {
+        if (pos >= L) return;
+        int op = op_at(pos);
+        if ((unsigned)op >= (unsigned)two_n) { bad = true; op = 0; }
+        const int a = pos == 0 ? 0 : op_customer(safe(op_at(pos - 1)));
+        const int64_t idx = (int64_t)a * I.W + op_customer(op);
+        if (INTD) cp_async4(rl + (pos & (LEG_SLOTS - 1)), I.d32 + idx);
+        else cp_async8(rl + (pos & (LEG_SLOTS - 1)), I.d + idx);
     }
-    __device__ __forceinline__ double leg0() const { return (double)l[0]; }
-    __device__ __forceinline__ void init(const DevInstance &I, const OpT *route, int len, int n2) {
-        rp = route; L = len; i = 0; two_n = n2; bad = false;
-#pragma unroll
-        for (int q = 0; q < OPS_AHEAD; ++q) o[q] = fetch(q);
-#pragma unroll
-        for (int q = 0; q < LEGS_AHEAD; ++q) o[q] = checked(o[q], q);
-        l[0] = leg(I, -1, o[0]);
-#pragma unroll
-        for (int q = 1; q < LEGS_AHEAD; ++q) l[q] = leg(I, o[q - 1], o[q]);
+    __device__ __forceinline__ void init(const DevInstance &I, const OpT *ops, int64_t route_elem,
+                                         int len, int n2, unsigned char *ring) {
+        words = reinterpret_cast<const uint32_t *>(ops);
+        ge0 = route_elem; L = len; i = 0; two_n = n2; bad = false;
+        rw = reinterpret_cast<uint32_t *>(ring);
+        rl = reinterpret_cast<LT *>(ring + OP_WORDS * 4);
+        next_w = word_of(0);
+        last_w = len > 0 ? word_of(len - 1) : next_w - 1;
+        for (int q = 0; q < OP_WORDS && next_w <= last_w; ++q) issue_word();
+        cp_commit();
+        cp_wait<0>();
+        for (int q = 0; q < LEG_AHEAD - 1; ++q) {
+            issue_leg(I, q);
+            cp_commit();
+        }
+    }
+    // wait for position i's leg; returns (op code, leg) of position i
+    __device__ __forceinline__ int cur_op() const { return safe(op_at(i)); }
+    __device__ __forceinline__ double cur_leg() const {
+        return (double)rl[i & (LEG_SLOTS - 1)];
     }
     __device__ __forceinline__ void advance(const DevInstance &I) {
         ++i;
-#pragma unroll
-        for (int q = 0; q + 1 < OPS_AHEAD; ++q) o[q] = o[q + 1];
-        o[OPS_AHEAD - 1] = fetch(i + OPS_AHEAD - 1);
-        o[LEGS_AHEAD - 1] = checked(o[LEGS_AHEAD - 1], i + LEGS_AHEAD - 1);
-#pragma unroll
-        for (int q = 0; q + 1 < LEGS_AHEAD; ++q) l[q] = l[q + 1];
-        l[LEGS_AHEAD - 1] = leg(I, o[LEGS_AHEAD - 2], o[LEGS_AHEAD - 1]);
+        if (next_w <= last_w && next_w < word_of(i) + OP_WORDS) issue_word();
+        issue_leg(I, i + LEG_AHEAD - 1);
+        cp_commit();
     }
-    // re-read and validate the op at `pos` (capacity scan past a deadlock)
-    __device__ __forceinline__ int checked_at(int pos) { return checked(fetch(pos), pos); }
 };
 
 template <typename OpT, bool INTD, int MODE, bool REC>
@@ -140,8 +169,10 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     const int wpb = blockDim.x >> 5;
     const int n = I.n, m = I.m, k = I.k, two_n = 2 * n;
     const CandLayout CL = cand_layout(n, MODE);
+    constexpr size_t RB = ring_bytes(INTD);
     double *s_p = reinterpret_cast<double *>(smem);
-    unsigned char *wbase = smem + block_p_bytes(n) + (size_t)warp * G * CL.total;
+    unsigned char *wbase = smem + block_p_bytes(n) + (size_t)warp * (G * CL.total + 32 * RB);
+    unsigned char *ring = wbase + (size_t)G * CL.total + (size_t)lane * RB;
 
     const int g = lane / m, v = lane - (lane / m) * m;
     const bool glane = g < G;
@@ -172,7 +203,6 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             }
             mal |= total > two_n || total > stride || (MODE != MODE_EXACT && total != two_n);
         }
-        const OpT *row = ops + (live ? cand : 0) * stride;
 
         // ---- shared tables: ready = -1 (dropoff not done); validation bitmap
         for (int gg = 0; gg < G; ++gg) {
@@ -208,7 +238,8 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         const bool run = live && !mal;
 
         RouteStream<OpT, INTD> rs;
-        rs.init(I, row + off, run ? L : 0, two_n);
+        const int64_t route_elem = (live ? cand : 0) * stride + off;
+        rs.init(I, ops, route_elem, run ? L : 0, two_n, ring);
         double t = 0.0;
         int s = 0, lo = 0, hi = k, lastc = 0;
         bool dead = false, bad_ops = false;
@@ -216,9 +247,10 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         if (MODE == MODE_TWO) {
             // pass 1: no-wait walk; ready = dropoff time + p (schedule.py:371-378)
             while (rs.i < rs.L) {
-                const int op = rs.o[0];
+                cp_wait<LEG_AHEAD - 1>();
+                const int op = rs.cur_op();
                 const int c = op_customer(op);
-                t = t + rs.leg0();
+                t = t + rs.cur_leg();
                 if (!(op & 1)) {
                     s_ready[c] = t + s_p[c];
                     s_posd[c] = ((uint32_t)v << 16) | (uint32_t)rs.i;
@@ -231,12 +263,14 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             __syncwarp();
             // pass 2: waits at pickups (schedule.py:380-393), and the same-route
             // pickup-before-its-dropoff Deadlock (:362-369)
-            rs.init(I, row + off, run ? L : 0, two_n);
+            cp_wait<0>();
+            rs.init(I, ops, route_elem, run ? L : 0, two_n, ring);
             t = 0.0;
             while (rs.i < rs.L) {
-                const int op = rs.o[0];
+                cp_wait<LEG_AHEAD - 1>();
+                const int op = rs.cur_op();
                 const int c = op_customer(op);
-                t = t + rs.leg0();
+                t = t + rs.cur_leg();
                 if (op & 1) {
                     const double r = s_ready[c];
                     if (r > t) t = r;
@@ -248,13 +282,14 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         } else {
             for (;;) {
                 const bool active = run && !dead && rs.i < rs.L;
-                const int op = active ? rs.o[0] : 0;
+                cp_wait<LEG_AHEAD - 1>();
+                const int op = active ? rs.cur_op() : 0;
                 const int c = op_customer(op);
                 const bool pick = op & 1;
                 const double r = s_ready[c];
                 const double pc = s_p[c];
                 const bool go = active && !(pick && r < 0.0);
-                const double arr = t + rs.leg0();
+                const double arr = t + (active ? rs.cur_leg() : 0.0);
                 const double tn = (pick && !(arr >= r)) ? r : arr;
                 if (go) {
                     if (!pick) s_ready[c] = tn + pc;
@@ -275,7 +310,11 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 if ((left & gmask) && !(moved & gmask)) dead = true;  // this candidate is stuck
             }
             if (dead)  // finish the capacity test past the stuck position
-                for (int j = rs.i; j < rs.L; ++j) cap_step(rs.checked_at(j), k, s, lo, hi);
+                for (int j = rs.i; j < rs.L; ++j) {
+                    const int op = (int)__ldg(ops + route_elem + j);
+                    if ((unsigned)op >= (unsigned)two_n) rs.bad = true;
+                    cap_step(op, k, s, lo, hi);
+                }
             bad_ops = rs.bad;
         }
         mal = mal || ((__ballot_sync(VRP_FULL_MASK, live && bad_ops) & gmask) != 0);
@@ -298,6 +337,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         }
         if (live && returns_out) returns_out[cand * m + v] = st == ST_OK ? ret : 0.0;
         if (REC && live && q0_out) q0_out[cand * m + v] = lo;
+        cp_wait<0>();  // the ring is reused by the next batch
         __syncwarp();
     }
 }
@@ -309,14 +349,15 @@ struct Shape {
 };
 
 template <typename Kern>
-int plan(Kern kern, int n, int m, int mode, Shape &out) {
+int plan(Kern kern, int n, int m, int mode, bool intd, Shape &out) {
     const size_t per_cand = cand_layout(n, mode).total;
     const size_t pbytes = block_p_bytes(n);
+    const size_t rbytes = 32 * ring_bytes(intd);
     const int gmax = 32 / m;
     long best = -1;
     for (int G = gmax; G >= 1; --G) {
         for (int w = 8; w >= 1; --w) {
-            const size_t bytes = pbytes + (size_t)w * G * per_cand;
+            const size_t bytes = pbytes + (size_t)w * (G * per_cand + rbytes);
             if (bytes > 227 * 1024) continue;
             if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
                 return -1;
@@ -340,7 +381,7 @@ int launch_t(const DevInstance &I, const void *ops, int64_t stride, const int32_
     static int cached_n = -1, cached_m = -1;
     static Shape sh;
     if (cached_n != I.n || cached_m != I.m) {
-        const int rc = plan(kern, I.n, I.m, MODE, sh);
+        const int rc = plan(kern, I.n, I.m, MODE, INTD, sh);
         if (rc) return rc;
         cached_n = I.n;
         cached_m = I.m;
