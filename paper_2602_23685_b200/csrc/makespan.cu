@@ -66,9 +66,10 @@ __device__ __forceinline__ void cap_step(int op, int k, int &s, int &lo, int &hi
 // ring filled by cp.async (LDGSTS): op words (4 B = 2 int16 or 1 int32 op
 // codes) are issued OP_WORDS words ahead, legs d[prev][c] are gathered
 // LEG_AHEAD positions ahead into LEG_SLOTS slots.  Every advance commits one
-// async group; consuming position i first waits until at most LEG_AHEAD-1
-// groups are pending, which covers the leg of position i (committed LEG_AHEAD-1
-// advances ago) and every op word that can be read (OP_WORDS >= 2*LEG_AHEAD).
+// async group (advancing to i gathers the leg of i+LEG_AHEAD-1); consuming
+// position i first waits until at most LEG_AHEAD-1 groups are pending -- those
+// hold legs i+1 .. i+LEG_AHEAD-1, so the leg of i has landed, and so has every
+// op word that can be read (OP_WORDS >= 2*LEG_AHEAD).
 // No register ever waits on an in-flight load, so the walk's per-iteration
 // latency is only its own dependency chain.  Out-of-range op codes set `bad`
 // and read as op 0 so that no gather leaves the matrix.
@@ -138,7 +139,7 @@ struct RouteStream {
         for (int q = 0; q < OP_WORDS && next_w <= last_w; ++q) issue_word();
         cp_commit();
         cp_wait<0>();
-        for (int q = 0; q < LEG_AHEAD - 1; ++q) {
+        for (int q = 0; q < LEG_AHEAD; ++q) {  // legs of positions 0 .. LEG_AHEAD-1
             issue_leg(I, q);
             cp_commit();
         }
