@@ -96,47 +96,42 @@ __host__ __device__ constexpr size_t ring_bytes(bool intd) {
 template <typename OpT, bool INTD>
 struct RouteStream {
     using LT = typename std::conditional<INTD, int32_t, double>::type;
-    static constexpr int E = sizeof(OpT) == 2 ? 2 : 1;  // op codes per 4-byte word
-    const uint32_t *words;  // ops buffer viewed as 4-byte words
-    int64_t ge0;            // element index of route position 0
+    static constexpr int SH = sizeof(OpT) == 2 ? 1 : 0;  // log2(op codes per 4-byte word)
+    const uint32_t *wp;  // first word holding this route's ops
+    int par;             // element offset of position 0 inside word 0 (int16 only)
     int L, i, two_n;
-    int64_t next_w, last_w; // next word to issue, last word of the route
-    uint32_t *rw;           // ring: op words
-    LT *rl;                 // ring: legs
+    int nw, lastw;       // next word to issue / last word of the route (relative to wp)
+    int gprev;           // op code of the last position whose leg was issued (-1: depot)
+    uint32_t *rw;        // ring: op words
+    LT *rl;              // ring: legs
     bool bad;
 
-    __device__ __forceinline__ int64_t word_of(int pos) const { return (ge0 + pos) / E; }
-    __device__ __forceinline__ void issue_word() {
-        cp_async4(rw + (next_w & (OP_WORDS - 1)), words + next_w);
-        ++next_w;
-    }
-    // op code at route position pos (its word must have landed); -1 past the end
-    __device__ __forceinline__ int op_at(int pos) const {
-        if (pos >= L) return -1;
-        const int64_t ge = ge0 + pos;
-        const uint32_t w = rw[(ge / E) & (OP_WORDS - 1)];
-        if (E == 2) return (int)(int16_t)(w >> ((ge & 1) * 16));
+    __device__ __forceinline__ int op_at(int p) const {
+        const int e = par + p;
+        const uint32_t w = rw[(e >> SH) & (OP_WORDS - 1)];
+        if (SH) return (int)(int16_t)(w >> ((e & 1) << 4));
         return (int)w;
     }
-    __device__ __forceinline__ int safe(int op) const { return (unsigned)op < (unsigned)two_n ? op : 0; }
-    __device__ __forceinline__ void issue_leg(const DevInstance &I, int pos) {
-        if (pos >= L) return;
-        int op = op_at(pos);
+    __device__ __forceinline__ void issue_leg(const DevInstance &I, int p) {
+        if (p >= L) return;
+        int op = op_at(p);
         if ((unsigned)op >= (unsigned)two_n) { bad = true; op = 0; }
-        const int a = pos == 0 ? 0 : op_customer(safe(op_at(pos - 1)));
-        const int64_t idx = (int64_t)a * I.W + op_customer(op);
-        if (INTD) cp_async4(rl + (pos & (LEG_SLOTS - 1)), I.d32 + idx);
-        else cp_async8(rl + (pos & (LEG_SLOTS - 1)), I.d + idx);
+        const int a = gprev < 0 ? 0 : op_customer(gprev);
+        gprev = op;
+        const int idx = a * I.W + op_customer(op);
+        if (INTD) cp_async4(rl + (p & (LEG_SLOTS - 1)), I.d32 + idx);
+        else cp_async8(rl + (p & (LEG_SLOTS - 1)), I.d + idx);
     }
     __device__ __forceinline__ void init(const DevInstance &I, const OpT *ops, int64_t route_elem,
                                          int len, int n2, unsigned char *ring) {
-        words = reinterpret_cast<const uint32_t *>(ops);
-        ge0 = route_elem; L = len; i = 0; two_n = n2; bad = false;
+        wp = reinterpret_cast<const uint32_t *>(ops) + (route_elem >> SH);
+        par = SH ? (int)(route_elem & 1) : 0;
+        L = len; i = 0; two_n = n2; bad = false; gprev = -1;
         rw = reinterpret_cast<uint32_t *>(ring);
         rl = reinterpret_cast<LT *>(ring + OP_WORDS * 4);
-        next_w = word_of(0);
-        last_w = len > 0 ? word_of(len - 1) : next_w - 1;
-        for (int q = 0; q < OP_WORDS && next_w <= last_w; ++q) issue_word();
+        nw = 0;
+        lastw = len > 0 ? (par + len - 1) >> SH : -1;
+        for (; nw < OP_WORDS && nw <= lastw; ++nw) cp_async4(rw + nw, wp + nw);
         cp_commit();
         cp_wait<0>();
         for (int q = 0; q < LEG_AHEAD; ++q) {  // legs of positions 0 .. LEG_AHEAD-1
@@ -144,14 +139,17 @@ struct RouteStream {
             cp_commit();
         }
     }
-    // wait for position i's leg; returns (op code, leg) of position i
-    __device__ __forceinline__ int cur_op() const { return safe(op_at(i)); }
-    __device__ __forceinline__ double cur_leg() const {
-        return (double)rl[i & (LEG_SLOTS - 1)];
+    __device__ __forceinline__ int cur_op() const {
+        const int op = op_at(i);
+        return (unsigned)op < (unsigned)two_n ? op : 0;
     }
+    __device__ __forceinline__ double cur_leg() const { return (double)rl[i & (LEG_SLOTS - 1)]; }
     __device__ __forceinline__ void advance(const DevInstance &I) {
         ++i;
-        if (next_w <= last_w && next_w < word_of(i) + OP_WORDS) issue_word();
+        if (nw <= lastw && nw < ((par + i) >> SH) + OP_WORDS) {
+            cp_async4(rw + (nw & (OP_WORDS - 1)), wp + nw);
+            ++nw;
+        }
         issue_leg(I, i + LEG_AHEAD - 1);
         cp_commit();
     }
