@@ -66,14 +66,14 @@ __device__ __forceinline__ void cap_step(int op, int k, int &s, int &lo, int &hi
 // ring filled by cp.async (LDGSTS): op words (4 B = 2 int16 or 1 int32 op
 // codes) are issued OP_WORDS words ahead, legs d[prev][c] are gathered
 // LEG_AHEAD positions ahead into LEG_SLOTS slots.  Every advance commits one
-// async group (advancing to i gathers the leg of i+LEG_AHEAD-1); consuming
-// position i first waits until at most LEG_AHEAD-1 groups are pending -- those
-// hold legs i+1 .. i+LEG_AHEAD-1, so the leg of i has landed, and so has every
-// op word that can be read (OP_WORDS >= 2*LEG_AHEAD).
+// async group (advancing to i gathers the leg of i+LEG_AHEAD-1); the walk at
+// position i waits until at most LEG_AHEAD-2 groups are pending -- those hold
+// legs i+2 .. i+LEG_AHEAD-1, so the legs of i and i+1 have landed, and so has
+// every op word that can be read (OP_WORDS >= 2*LEG_AHEAD).
 // No register ever waits on an in-flight load, so the walk's per-iteration
 // latency is only its own dependency chain.  Out-of-range op codes set `bad`
 // and read as op 0 so that no gather leaves the matrix.
-constexpr int LEG_AHEAD = 6;
+constexpr int LEG_AHEAD = 8;
 constexpr int LEG_SLOTS = 8;   // power of two >= LEG_AHEAD
 constexpr int OP_WORDS = 16;   // power of two >= 2 * LEG_AHEAD
 
@@ -139,11 +139,14 @@ struct RouteStream {
             cp_commit();
         }
     }
-    __device__ __forceinline__ int cur_op() const {
-        const int op = op_at(i);
+    // sanitised op code / leg of position p (p < L; its leg must have landed)
+    __device__ __forceinline__ int op_safe(int p) const {
+        const int op = op_at(p);
         return (unsigned)op < (unsigned)two_n ? op : 0;
     }
-    __device__ __forceinline__ double cur_leg() const { return (double)rl[i & (LEG_SLOTS - 1)]; }
+    __device__ __forceinline__ double leg_at(int p) const { return (double)rl[p & (LEG_SLOTS - 1)]; }
+    __device__ __forceinline__ int cur_op() const { return op_safe(i); }
+    __device__ __forceinline__ double cur_leg() const { return leg_at(i); }
     __device__ __forceinline__ void advance(const DevInstance &I) {
         ++i;
         if (nw <= lastw && nw < ((par + i) >> SH) + OP_WORDS) {
@@ -279,16 +282,23 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 rs.advance(I);
             }
         } else {
+            // software-pipelined: (op, leg) of position i+1 are decoded while
+            // position i runs its ready-table chain
+            cp_wait<LEG_AHEAD - 2>();
+            int op = rs.L > 0 ? rs.cur_op() : 0;
+            double lg = rs.L > 0 ? rs.cur_leg() : 0.0;
             for (;;) {
                 const bool active = run && !dead && rs.i < rs.L;
-                cp_wait<LEG_AHEAD - 1>();
-                const int op = active ? rs.cur_op() : 0;
-                const int c = op_customer(op);
-                const bool pick = op & 1;
+                cp_wait<LEG_AHEAD - 2>();  // legs of i and i+1 have landed
+                const bool has_next = rs.i + 1 < rs.L;
+                const int op_n = has_next ? rs.op_safe(rs.i + 1) : 0;
+                const double lg_n = has_next ? rs.leg_at(rs.i + 1) : 0.0;
+                const int c = op_customer(active ? op : 0);
+                const bool pick = active && (op & 1);
                 const double r = s_ready[c];
                 const double pc = s_p[c];
                 const bool go = active && !(pick && r < 0.0);
-                const double arr = t + (active ? rs.cur_leg() : 0.0);
+                const double arr = t + lg;
                 const double tn = (pick && !(arr >= r)) ? r : arr;
                 if (go) {
                     if (!pick) s_ready[c] = tn + pc;
@@ -301,6 +311,8 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                     lastc = c;
                     cap_step(op, k, s, lo, hi);
                     rs.advance(I);
+                    op = op_n;
+                    lg = lg_n;
                 }
                 const unsigned moved = __ballot_sync(VRP_FULL_MASK, go);
                 const unsigned left = __ballot_sync(VRP_FULL_MASK, active && rs.i < rs.L);
