@@ -93,9 +93,17 @@ __host__ __device__ constexpr size_t ring_bytes(bool intd) {
     return (size_t)OP_WORDS * 4 + (size_t)LEG_SLOTS * (intd ? 4 : 8);
 }
 
+// Event-time arithmetic: integral instances (every d and p an integer < 2^31,
+// all TSPLIB types) keep times in int64 -- exact, hence bit-identical to the
+// reference's fp64 sums, with short ALU latencies on the walk's critical
+// path; other instances use fp64 in the reference's operation order.
+template <bool INTD>
+using TimeT = typename std::conditional<INTD, long long, double>::type;
+
 template <typename OpT, bool INTD>
 struct RouteStream {
     using LT = typename std::conditional<INTD, int32_t, double>::type;
+    using TT = TimeT<INTD>;
     static constexpr int SH = sizeof(OpT) == 2 ? 1 : 0;  // log2(op codes per 4-byte word)
     const uint32_t *wp;  // first word holding this route's ops
     int par;             // element offset of position 0 inside word 0 (int16 only)
@@ -144,9 +152,9 @@ struct RouteStream {
         const int op = op_at(p);
         return (unsigned)op < (unsigned)two_n ? op : 0;
     }
-    __device__ __forceinline__ double leg_at(int p) const { return (double)rl[p & (LEG_SLOTS - 1)]; }
+    __device__ __forceinline__ TT leg_at(int p) const { return (TT)rl[p & (LEG_SLOTS - 1)]; }
     __device__ __forceinline__ int cur_op() const { return op_safe(i); }
-    __device__ __forceinline__ double cur_leg() const { return leg_at(i); }
+    __device__ __forceinline__ TT cur_leg() const { return leg_at(i); }
     __device__ __forceinline__ void advance(const DevInstance &I) {
         ++i;
         if (nw <= lastw && nw < ((par + i) >> SH) + OP_WORDS) {
@@ -172,7 +180,8 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     const int n = I.n, m = I.m, k = I.k, two_n = 2 * n;
     const CandLayout CL = cand_layout(n, MODE);
     constexpr size_t RB = ring_bytes(INTD);
-    double *s_p = reinterpret_cast<double *>(smem);
+    using TT = TimeT<INTD>;
+    TT *s_p = reinterpret_cast<TT *>(smem);
     unsigned char *wbase = smem + block_p_bytes(n) + (size_t)warp * (G * CL.total + 32 * RB);
     unsigned char *ring = wbase + (size_t)G * CL.total + (size_t)lane * RB;
 
@@ -181,10 +190,10 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     const unsigned gmask = glane ? (((m == 32) ? 0xffffffffu : ((1u << m) - 1u)) << (g * m)) : 0u;
     const int leader = g * m;  // lane holding route 0 of this lane's candidate
     unsigned char *cbase = wbase + (size_t)(glane ? g : 0) * CL.total;
-    double *s_ready = reinterpret_cast<double *>(cbase + CL.ready);
+    TT *s_ready = reinterpret_cast<TT *>(cbase + CL.ready);
     uint32_t *s_posd = reinterpret_cast<uint32_t *>(cbase + CL.posd);
 
-    for (int c = threadIdx.x; c <= n; c += blockDim.x) s_p[c] = __ldg(I.p + c);
+    for (int c = threadIdx.x; c <= n; c += blockDim.x) s_p[c] = INTD ? (TT)__ldg(I.p32 + c) : (TT)__ldg(I.p + c);
     __syncthreads();
 
     const int64_t step = (int64_t)gridDim.x * wpb * G;
@@ -208,8 +217,8 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
 
         // ---- shared tables: ready = -1 (dropoff not done); validation bitmap
         for (int gg = 0; gg < G; ++gg) {
-            double *rd = reinterpret_cast<double *>(wbase + (size_t)gg * CL.total + CL.ready);
-            for (int c = lane; c <= n; c += 32) rd[c] = -1.0;
+            TT *rd = reinterpret_cast<TT *>(wbase + (size_t)gg * CL.total + CL.ready);
+            for (int c = lane; c <= n; c += 32) rd[c] = (TT)-1;
             if (MODE != MODE_EXACT) {
                 uint32_t *bt = reinterpret_cast<uint32_t *>(wbase + (size_t)gg * CL.total + CL.bits);
                 for (int w = lane; w < (two_n + 31) / 32; w += 32) bt[w] = 0u;
@@ -242,7 +251,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         RouteStream<OpT, INTD> rs;
         const int64_t route_elem = (live ? cand : 0) * stride + off;
         rs.init(I, ops, route_elem, run ? L : 0, two_n, ring);
-        double t = 0.0;
+        TT t = 0;
         int s = 0, lo = 0, hi = k, lastc = 0;
         bool dead = false, bad_ops = false;
 
@@ -267,14 +276,14 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             // pickup-before-its-dropoff Deadlock (:362-369)
             cp_wait<0>();
             rs.init(I, ops, route_elem, run ? L : 0, two_n, ring);
-            t = 0.0;
+            t = 0;
             while (rs.i < rs.L) {
                 cp_wait<LEG_AHEAD - 1>();
                 const int op = rs.cur_op();
                 const int c = op_customer(op);
                 t = t + rs.cur_leg();
                 if (op & 1) {
-                    const double r = s_ready[c];
+                    const TT r = s_ready[c];
                     if (r > t) t = r;
                     const uint32_t pd = s_posd[c];
                     dead |= (int)(pd >> 16) == v && (int)(pd & 0xffffu) > rs.i;
@@ -286,26 +295,26 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             // position i runs its ready-table chain
             cp_wait<LEG_AHEAD - 2>();
             int op = rs.L > 0 ? rs.cur_op() : 0;
-            double lg = rs.L > 0 ? rs.cur_leg() : 0.0;
+            TT lg = rs.L > 0 ? rs.cur_leg() : (TT)0;
             for (;;) {
                 const bool active = run && !dead && rs.i < rs.L;
                 cp_wait<LEG_AHEAD - 2>();  // legs of i and i+1 have landed
                 const bool has_next = rs.i + 1 < rs.L;
                 const int op_n = has_next ? rs.op_safe(rs.i + 1) : 0;
-                const double lg_n = has_next ? rs.leg_at(rs.i + 1) : 0.0;
+                const TT lg_n = has_next ? rs.leg_at(rs.i + 1) : (TT)0;
                 const int c = op_customer(active ? op : 0);
                 const bool pick = active && (op & 1);
-                const double r = s_ready[c];
-                const double pc = s_p[c];
-                const bool go = active && !(pick && r < 0.0);
-                const double arr = t + lg;
-                const double tn = (pick && !(arr >= r)) ? r : arr;
+                const TT r = s_ready[c];
+                const TT pc = s_p[c];
+                const bool go = active && !(pick && r < (TT)0);
+                const TT arr = t + lg;
+                const TT tn = (pick && !(arr >= r)) ? r : arr;
                 if (go) {
                     if (!pick) s_ready[c] = tn + pc;
                     if (REC) {
                         const int64_t at = cand * stride + off + rs.i;
-                        arrival_out[at] = arr;
-                        time_out[at] = tn;
+                        arrival_out[at] = (double)arr;
+                        time_out[at] = (double)tn;
                     }
                     t = tn;
                     lastc = c;
@@ -334,7 +343,10 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         const int st = mal ? ST_MAL : (capfail ? ST_CAP : (gdead ? ST_DEAD : ST_OK));
 
         double ret = 0.0;
-        if (live && st == ST_OK && L > 0) ret = t + dist<INTD>(I, lastc, 0);
+        if (live && st == ST_OK && L > 0) {
+            if (INTD) ret = (double)(t + (TT)__ldg(I.d32 + (int64_t)lastc * I.W));
+            else ret = (double)t + __ldg(I.d + (int64_t)lastc * I.W);
+        }
         double z = 0.0;  // returns are >= 0; empty routes count as 0
         for (int u = 0; u < m; ++u) {
             const double x = __shfl_sync(VRP_FULL_MASK, ret, glane ? leader + u : lane);
