@@ -1,31 +1,27 @@
 // makespan.cu -- K1 (exact event-driven makespan, schedule.py:188-316) and
 // K2 (two-pass estimate, schedule.py:345-393) over batches of candidates.
 //
-// Mapping.  A warp carries G = floor(32/m) candidates at once; lane g*m+v owns
-// route v of candidate g (30 of 32 lanes busy for m = 6).  Persistent grid.
+// Mapping: a warp carries G = floor(32/m) candidates at once, lane g*m+v owns
+// route v of candidate g (30 of 32 lanes busy for m = 6); persistent grid.
 //
-// Windowed staging.  Each route has a WIN-position window in shared memory
-// holding its op codes and legs d[prev][c].  Whenever some lane has consumed
-// the older half of its window, the WHOLE WARP refills: for up to
-// REFILL_BATCH routes at a time, 32 lanes stream the next CHUNK op codes of a
-// route (coalesced), exchange the predecessor op with a shuffle and gather the
-// legs from the L2-resident matrix -- all loads of a round are issued before
-// any is consumed.  Refills are warp-uniform (no divergence) and the per-lane
-// replay loop below touches shared memory only.  Per candidate this costs the
-// ready table (8(n+1) B) plus m*WIN*(4+2) B of window, ~10 KB at n = 999, so
-// ~20 candidates are in flight per SM.
+// Each lane streams its own route through a register pipeline -- op codes
+// loaded OPS_AHEAD positions ahead (read-only path, L1 line reuse), legs
+// d[prev][c] gathered from the L2-resident matrix LEGS_AHEAD positions ahead --
+// so the only shared memory a candidate needs is its ready table
+// ready[c] = t_drop[c] + p[c] (fp64, n+1 slots) plus one block-shared copy of
+// p.  That keeps ~25 candidates in flight per SM at n = 999.
 //
 // Replay (exact / evaluate): lockstep dataflow.  Every iteration each lane
 // executes the next op of its route unless it is a pickup whose dropoff has
 // not happened yet (ready < 0):
 //     dropoff  t = t + leg;                 ready[c] = t + p[c]
 //     pickup   arr = t + leg;  t = arr >= ready[c] ? arr : ready[c]
-// Writes become visible to the other lanes at the __syncwarp() ending the
+// Writes become visible to the other lanes at the __syncwarp() closing the
 // iteration, so the iteration count is the depth of the precedence DAG.  A
 // candidate whose lanes all stall while ops remain is a circular wait
 // (Deadlock, schedule.py:243-245 / :308-309).  Each value depends only on its
-// DAG predecessors; integral instances keep times in int64 (exact), others in
-// fp64 with the reference's operation order -- bit-identical either way.
+// DAG predecessors and is computed with the reference's fp64 operation order,
+// so results are bit-identical to the reference's round-robin replay.
 //
 // Capacity (route_initial_load, schedule.py:159-185) is the running interval
 // [lo, hi] of feasible initial loads; lo only grows and hi only shrinks, so
@@ -41,113 +37,105 @@ namespace {
 
 constexpr int MODE_EXACT = 0, MODE_EVAL = 1, MODE_TWO = 2;
 constexpr int ST_OK = 0, ST_CAP = 1, ST_DEAD = 2, ST_MAL = 3;
-constexpr int WIN = 64;           // staged positions per route (power of two)
-constexpr int CHUNK = 32;         // positions staged per refill (= warp width)
-constexpr int REFILL_BATCH = 4;   // routes refilled per round (loads in flight)
+constexpr int OPS_AHEAD = 8;   // op codes in registers (positions i .. i+7)
+constexpr int LEGS_AHEAD = 4;  // gathered legs in registers (positions i .. i+3)
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-template <bool INTD>
-using TimeT = typename std::conditional<INTD, long long, double>::type;  // event times
-template <bool INTD>
-using LegT = typename std::conditional<INTD, int32_t, double>::type;     // staged legs
-
-// Per candidate: ready table, route windows, plus (validating modes) an op
-// bitmap and (two-pass) the (route, position) of every dropoff.
+// Per candidate: ready table, plus (validating modes) an op bitmap and (two-
+// pass) the (route, position) of every dropoff.
 struct CandLayout {
-    size_t ready, wleg, wop, bits, posd, total;
+    size_t ready, bits, posd, total;
 };
 
-__host__ __device__ inline CandLayout cand_layout(int n, int m, bool intd, int mode) {
+__host__ __device__ inline CandLayout cand_layout(int n, int mode) {
     CandLayout L;
     size_t o = 0;
-    L.ready = o; o += align16(8 * (size_t)(n + 1));
-    L.wleg = o;  o += align16((intd ? 4 : 8) * (size_t)m * WIN);
-    L.wop = o;   o += align16(2 * (size_t)m * WIN);
-    L.bits = o;  if (mode != MODE_EXACT) o += align16(4 * (size_t)((2 * n + 31) / 32));
-    L.posd = o;  if (mode == MODE_TWO) o += align16(4 * (size_t)(n + 1));
+    L.ready = o; o += align16(sizeof(double) * (size_t)(n + 1));
+    L.bits = o;  if (mode != MODE_EXACT) o += align16(sizeof(uint32_t) * (size_t)((2 * n + 31) / 32));
+    L.posd = o;  if (mode == MODE_TWO) o += align16(sizeof(uint32_t) * (size_t)(n + 1));
     L.total = o;
     return L;
 }
 
-__host__ __device__ inline size_t block_p_bytes(int n) { return align16(8 * (size_t)(n + 1)); }
+__host__ __device__ inline size_t block_p_bytes(int n) { return align16(sizeof(double) * (size_t)(n + 1)); }
 
 __device__ __forceinline__ void cap_step(int op, int k, int &s, int &lo, int &hi) {
     if (op & 1) { int room = k - 1 - s; hi = room < hi ? room : hi; ++s; }
     else        { int need = 1 - s;     lo = need > lo ? need : lo; --s; }
 }
 
-// Per-lane view of its route.
-struct Route {
-    int64_t re;   // element index of position 0 in the ops buffer
-    int L;        // length
-    int i;        // next position to execute
-    int staged;   // positions [staged - WIN, staged) are in the window
-};
+// One route's op codes and legs, streamed through registers.  Loads enter at
+// the back of the pipeline and are only consumed stages later, so neither the
+// op load (L1) nor the leg gather (L2) sits on the per-iteration critical
+// path: an op code is range-checked when it reaches the gather stage
+// (LEGS_AHEAD-1), a gathered leg is converted to fp64 when it reaches stage 0.
+// Positions past the end read as -1; out-of-range codes set `bad` and are
+// replaced by op 0 so that no gather leaves the matrix.
+template <bool INTD>
+struct LegRaw { using T = double; };
+template <>
+struct LegRaw<true> { using T = int32_t; };
 
-// Stage the next CHUNK positions of every route in `need` (a lane mask),
-// REFILL_BATCH routes per round.  Warp-uniform; returns (uniformly) the lanes
-// whose newly staged op codes were out of range.
+template <bool INTD>
+__device__ __forceinline__ typename LegRaw<INTD>::T gather_leg(const DevInstance &I, int a, int b) {
+    // L2-only load: the random d gathers must not evict the op-stream lines from L1
+    if (INTD) return (typename LegRaw<INTD>::T)__ldcg(I.d32 + (int64_t)a * I.W + b);
+    return (typename LegRaw<INTD>::T)__ldcg(I.d + (int64_t)a * I.W + b);
+}
+
+// Event-time arithmetic: integral instances (every d and p an integer < 2^31,
+// all TSPLIB types) keep times in int64 -- exact, hence bit-identical to the
+// reference's fp64 sums, with short ALU latencies on the replay's critical
+// path; other instances use fp64 in the reference's operation order.
+template <bool INTD>
+using TimeT = typename std::conditional<INTD, long long, double>::type;
+
 template <typename OpT, bool INTD>
-__device__ __forceinline__ unsigned refill(const DevInstance &I, const OpT *__restrict__ ops,
-                                           unsigned need, Route &R, int lane, int m,
-                                           unsigned char *wbase, const CandLayout &CL, int two_n) {
-    using LT = LegT<INTD>;
-    unsigned badmask = 0;
-    while (need) {
-        int rl[REFILL_BATCH], pos[REFILL_BATCH], op[REFILL_BATCH];
-        unsigned served = 0;
-#pragma unroll
-        for (int b = 0; b < REFILL_BATCH; ++b) {
-            rl[b] = need ? __ffs(need) - 1 : -1;
-            if (rl[b] >= 0) { served |= 1u << rl[b]; need &= need - 1; }
-        }
-        // op codes: coalesced; every round's loads in flight together
-#pragma unroll
-        for (int b = 0; b < REFILL_BATCH; ++b) {
-            const int src = rl[b] < 0 ? lane : rl[b];
-            const int s = __shfl_sync(VRP_FULL_MASK, R.staged, src);
-            const int L = __shfl_sync(VRP_FULL_MASK, R.L, src);
-            const long long re = __shfl_sync(VRP_FULL_MASK, (long long)R.re, src);
-            pos[b] = s + lane;
-            const bool ok = rl[b] >= 0 && pos[b] < L;
-            op[b] = ok ? (int)__ldg(ops + re + pos[b]) : -1;
-            if (!ok) pos[b] = -1;
-        }
-        LT leg[REFILL_BATCH];
-#pragma unroll
-        for (int b = 0; b < REFILL_BATCH; ++b) {
-            const int src = rl[b] < 0 ? 0 : rl[b];
-            const int gg = src / m, vv = src - (src / m) * m;
-            const uint16_t *wop = reinterpret_cast<const uint16_t *>(wbase + (size_t)gg * CL.total + CL.wop) + vv * WIN;
-            const bool bad = pos[b] >= 0 && (unsigned)op[b] >= (unsigned)two_n;
-            if (bad) op[b] = 0;
-            if (__any_sync(VRP_FULL_MASK, bad) && rl[b] >= 0) badmask |= 1u << rl[b];
-            int prev = __shfl_up_sync(VRP_FULL_MASK, op[b], 1);
-            if (lane == 0) prev = pos[b] > 0 ? (int)wop[(pos[b] - 1) & (WIN - 1)] : -1;
-            const int a = prev < 0 ? 0 : op_customer(prev);
-            const int idx = a * I.W + op_customer(op[b] < 0 ? 0 : op[b]);
-            if (pos[b] >= 0) leg[b] = INTD ? (LT)__ldcg(I.d32 + idx) : (LT)__ldcg(I.d + idx);
-            else leg[b] = (LT)0;
-        }
-#pragma unroll
-        for (int b = 0; b < REFILL_BATCH; ++b) {
-            if (pos[b] < 0) continue;
-            const int gg = rl[b] / m, vv = rl[b] - (rl[b] / m) * m;
-            unsigned char *cb = wbase + (size_t)gg * CL.total;
-            reinterpret_cast<uint16_t *>(cb + CL.wop)[vv * WIN + (pos[b] & (WIN - 1))] = (uint16_t)op[b];
-            reinterpret_cast<LT *>(cb + CL.wleg)[vv * WIN + (pos[b] & (WIN - 1))] = leg[b];
-        }
-        if ((served >> lane) & 1u) R.staged += CHUNK;
-        __syncwarp();
-    }
-    return badmask;
-}
+struct RouteStream {
+    using LT = typename LegRaw<INTD>::T;
+    using TT = TimeT<INTD>;
+    const OpT *rp;
+    int L, i, two_n;
+    int o[OPS_AHEAD];
+    LT l[LEGS_AHEAD];
+    bool bad;
 
-// Lanes whose window can take (and still lacks) their next chunk.
-__device__ __forceinline__ bool wants_chunk(const Route &R, bool run) {
-    return run && R.staged < R.L && R.i >= R.staged - WIN + CHUNK;
-}
+    __device__ __forceinline__ int fetch(int pos) const { return pos < L ? (int)__ldg(rp + pos) : -1; }
+    // validate the op at route position `pos` (past the end -> -1 sentinel)
+    __device__ __forceinline__ int checked(int op, int pos) {
+        if (pos >= L) return -1;
+        if ((unsigned)op >= (unsigned)two_n) { bad = true; return 0; }
+        return op;
+    }
+    __device__ __forceinline__ LT leg(const DevInstance &I, int prev_op, int op) const {
+        if (op < 0) return (LT)0;
+        return gather_leg<INTD>(I, prev_op < 0 ? 0 : op_customer(prev_op), op_customer(op));
+    }
+    __device__ __forceinline__ TT leg0() const { return (TT)l[0]; }
+    __device__ __forceinline__ void init(const DevInstance &I, const OpT *route, int len, int n2) {
+        rp = route; L = len; i = 0; two_n = n2; bad = false;
+#pragma unroll
+        for (int q = 0; q < OPS_AHEAD; ++q) o[q] = fetch(q);
+#pragma unroll
+        for (int q = 0; q < LEGS_AHEAD; ++q) o[q] = checked(o[q], q);
+        l[0] = leg(I, -1, o[0]);
+#pragma unroll
+        for (int q = 1; q < LEGS_AHEAD; ++q) l[q] = leg(I, o[q - 1], o[q]);
+    }
+    __device__ __forceinline__ void advance(const DevInstance &I) {
+        ++i;
+#pragma unroll
+        for (int q = 0; q + 1 < OPS_AHEAD; ++q) o[q] = o[q + 1];
+        o[OPS_AHEAD - 1] = fetch(i + OPS_AHEAD - 1);
+        o[LEGS_AHEAD - 1] = checked(o[LEGS_AHEAD - 1], i + LEGS_AHEAD - 1);
+#pragma unroll
+        for (int q = 0; q + 1 < LEGS_AHEAD; ++q) l[q] = l[q + 1];
+        l[LEGS_AHEAD - 1] = leg(I, o[LEGS_AHEAD - 2], o[LEGS_AHEAD - 1]);
+    }
+    // re-read and validate the op at `pos` (capacity scan past a deadlock)
+    __device__ __forceinline__ int checked_at(int pos) { return checked(fetch(pos), pos); }
+};
 
 template <typename OpT, bool INTD, int MODE, bool REC>
 __global__ void __launch_bounds__(256)
@@ -156,14 +144,13 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 int32_t *__restrict__ status_out, double *__restrict__ returns_out,
                 int32_t *__restrict__ bottleneck_out, double *__restrict__ arrival_out,
                 double *__restrict__ time_out, int32_t *__restrict__ q0_out) {
-    using TT = TimeT<INTD>;
-    using LT = LegT<INTD>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int n = I.n, m = I.m, k = I.k, two_n = 2 * n;
-    const CandLayout CL = cand_layout(n, m, INTD, MODE);
+    const CandLayout CL = cand_layout(n, MODE);
+    using TT = TimeT<INTD>;
     TT *s_p = reinterpret_cast<TT *>(smem);
     unsigned char *wbase = smem + block_p_bytes(n) + (size_t)warp * G * CL.total;
 
@@ -174,8 +161,6 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     unsigned char *cbase = wbase + (size_t)(glane ? g : 0) * CL.total;
     TT *s_ready = reinterpret_cast<TT *>(cbase + CL.ready);
     uint32_t *s_posd = reinterpret_cast<uint32_t *>(cbase + CL.posd);
-    const LT *w_leg = reinterpret_cast<const LT *>(cbase + CL.wleg) + (glane ? v : 0) * WIN;
-    const uint16_t *w_op = reinterpret_cast<const uint16_t *>(cbase + CL.wop) + (glane ? v : 0) * WIN;
 
     for (int c = threadIdx.x; c <= n; c += blockDim.x)
         s_p[c] = INTD ? (TT)__ldg(I.p32 + c) : (TT)__ldg(I.p + c);
@@ -199,6 +184,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             }
             mal |= total > two_n || total > stride || (MODE != MODE_EXACT && total != two_n);
         }
+        const OpT *row = ops + (live ? cand : 0) * stride;
 
         // ---- shared tables: ready = -1 (dropoff not done); validation bitmap
         for (int gg = 0; gg < G; ++gg) {
@@ -233,103 +219,78 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         mal = (__ballot_sync(VRP_FULL_MASK, live && mal) & gmask) != 0;
         const bool run = live && !mal;
 
-        Route R;
-        R.re = (live ? cand : 0) * stride + off;
-        R.L = run ? L : 0;
-        R.i = 0;
-        R.staged = 0;
-        unsigned bad = 0;  // lanes whose route holds an out-of-range op code
+        RouteStream<OpT, INTD> rs;
+        rs.init(I, row + off, run ? L : 0, two_n);
         TT t = 0;
         int s = 0, lo = 0, hi = k, lastc = 0;
-        bool dead = false;
+        bool dead = false, bad_ops = false;
 
         if (MODE == MODE_TWO) {
             // pass 1: no-wait walk; ready = dropoff time + p (schedule.py:371-378)
-            for (;;) {
-                const unsigned need = __ballot_sync(VRP_FULL_MASK, wants_chunk(R, run));
-                if (need) bad |= refill<OpT, INTD>(I, ops, need, R, lane, m, wbase, CL, two_n);
-                const bool active = R.i < R.L;
-                if (!__any_sync(VRP_FULL_MASK, active)) break;
-                if (active) {
-                    const int slot = R.i & (WIN - 1);
-                    const int op = w_op[slot];
-                    const int c = op_customer(op);
-                    t = t + (TT)w_leg[slot];
-                    if (!(op & 1)) {
-                        s_ready[c] = t + s_p[c];
-                        s_posd[c] = ((uint32_t)v << 16) | (uint32_t)R.i;
-                    }
-                    cap_step(op, k, s, lo, hi);
-                    ++R.i;
+            while (rs.i < rs.L) {
+                const int op = rs.o[0];
+                const int c = op_customer(op);
+                t = t + rs.leg0();
+                if (!(op & 1)) {
+                    s_ready[c] = t + s_p[c];
+                    s_posd[c] = ((uint32_t)v << 16) | (uint32_t)rs.i;
                 }
+                cap_step(op, k, s, lo, hi);
+                lastc = c;
+                rs.advance(I);
             }
+            bad_ops = rs.bad;
             __syncwarp();
             // pass 2: waits at pickups (schedule.py:380-393), and the same-route
             // pickup-before-its-dropoff Deadlock (:362-369)
-            R.i = 0;
-            R.staged = 0;
+            rs.init(I, row + off, run ? L : 0, two_n);
             t = 0;
-            for (;;) {
-                const unsigned need = __ballot_sync(VRP_FULL_MASK, wants_chunk(R, run));
-                if (need) refill<OpT, INTD>(I, ops, need, R, lane, m, wbase, CL, two_n);
-                const bool active = R.i < R.L;
-                if (!__any_sync(VRP_FULL_MASK, active)) break;
-                if (active) {
-                    const int slot = R.i & (WIN - 1);
-                    const int op = w_op[slot];
-                    const int c = op_customer(op);
-                    t = t + (TT)w_leg[slot];
-                    if (op & 1) {
-                        const TT r = s_ready[c];
-                        if (r > t) t = r;
-                        const uint32_t pd = s_posd[c];
-                        dead |= (int)(pd >> 16) == v && (int)(pd & 0xffffu) > R.i;
-                    }
-                    lastc = c;
-                    ++R.i;
+            while (rs.i < rs.L) {
+                const int op = rs.o[0];
+                const int c = op_customer(op);
+                t = t + rs.leg0();
+                if (op & 1) {
+                    const TT r = s_ready[c];
+                    if (r > t) t = r;
+                    const uint32_t pd = s_posd[c];
+                    dead |= (int)(pd >> 16) == v && (int)(pd & 0xffffu) > rs.i;
                 }
+                rs.advance(I);
             }
         } else {
             for (;;) {
-                const unsigned need = __ballot_sync(VRP_FULL_MASK, wants_chunk(R, run && !dead));
-                if (need) bad |= refill<OpT, INTD>(I, ops, need, R, lane, m, wbase, CL, two_n);
-                const bool active = run && !dead && R.i < R.L;
-                const int slot = R.i & (WIN - 1);
-                const int op = active ? (int)w_op[slot] : 0;
-                const TT lg = (TT)w_leg[slot];
+                const bool active = run && !dead && rs.i < rs.L;
+                const int op = active ? rs.o[0] : 0;
                 const int c = op_customer(op);
                 const bool pick = op & 1;
                 const TT r = s_ready[c];
                 const TT pc = s_p[c];
                 const bool go = active && !(pick && r < (TT)0);
-                const TT arr = t + lg;
+                const TT arr = t + rs.leg0();
                 const TT tn = (pick && !(arr >= r)) ? r : arr;
                 if (go) {
                     if (!pick) s_ready[c] = tn + pc;
                     if (REC) {
-                        const int64_t at = R.re + R.i;
+                        const int64_t at = cand * stride + off + rs.i;
                         arrival_out[at] = (double)arr;
                         time_out[at] = (double)tn;
                     }
                     t = tn;
                     lastc = c;
                     cap_step(op, k, s, lo, hi);
-                    ++R.i;
+                    rs.advance(I);
                 }
                 const unsigned moved = __ballot_sync(VRP_FULL_MASK, go);
-                const unsigned left = __ballot_sync(VRP_FULL_MASK, active && R.i < R.L);
+                const unsigned left = __ballot_sync(VRP_FULL_MASK, active && rs.i < rs.L);
                 __syncwarp();
                 if (!left) break;
                 if ((left & gmask) && !(moved & gmask)) dead = true;  // this candidate is stuck
             }
             if (dead)  // finish the capacity test past the stuck position
-                for (int j = R.i; j < R.L; ++j) {
-                    const int op = (int)__ldg(ops + R.re + j);
-                    if ((unsigned)op >= (unsigned)two_n) bad |= 1u << lane;
-                    cap_step(op, k, s, lo, hi);
-                }
+                for (int j = rs.i; j < rs.L; ++j) cap_step(rs.checked_at(j), k, s, lo, hi);
+            bad_ops = rs.bad;
         }
-        mal = mal || ((__reduce_or_sync(VRP_FULL_MASK, bad) & gmask) != 0);
+        mal = mal || ((__ballot_sync(VRP_FULL_MASK, live && bad_ops) & gmask) != 0);
         const bool capfail = (__ballot_sync(VRP_FULL_MASK, live && lo > hi) & gmask) != 0;
         const bool gdead = (__ballot_sync(VRP_FULL_MASK, live && dead) & gmask) != 0;
         const int st = mal ? ST_MAL : (capfail ? ST_CAP : (gdead ? ST_DEAD : ST_OK));
@@ -363,8 +324,8 @@ struct Shape {
 };
 
 template <typename Kern>
-int plan(Kern kern, int n, int m, bool intd, int mode, Shape &out) {
-    const size_t per_cand = cand_layout(n, m, intd, mode).total;
+int plan(Kern kern, int n, int m, int mode, Shape &out) {
+    const size_t per_cand = cand_layout(n, mode).total;
     const size_t pbytes = block_p_bytes(n);
     const int gmax = 32 / m;
     long best = -1;
@@ -377,7 +338,7 @@ int plan(Kern kern, int n, int m, bool intd, int mode, Shape &out) {
             int blocks = 0;
             if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32 * w, bytes) != cudaSuccess)
                 return -1;
-            // most resident candidates; among equals, fewer warps (fewer issued instructions)
+            // most resident candidates; among equals, fewer warps (fewer instructions)
             const long score = (long)blocks * w * G * 64 - (long)blocks * w;
             if (blocks > 0 && score > best) { best = score; out = {G, w, blocks, bytes}; }
         }
@@ -394,7 +355,7 @@ int launch_t(const DevInstance &I, const void *ops, int64_t stride, const int32_
     static int cached_n = -1, cached_m = -1;
     static Shape sh;
     if (cached_n != I.n || cached_m != I.m) {
-        const int rc = plan(kern, I.n, I.m, INTD, MODE, sh);
+        const int rc = plan(kern, I.n, I.m, MODE, sh);
         if (rc) return rc;
         cached_n = I.n;
         cached_m = I.m;
