@@ -266,11 +266,13 @@ def run_gpu(args):
         achieved = per_eval * n_cand / (ms_per_step / 1e3) / 1e9  # per GPU, dominant kernel
         traffic = None
         tp = REPO / "profiles" / "k1_traffic.json"
-        if tp.exists():
-            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+        if tp.exists():  # ncu --set full capture of K1 (dram read+write), scaled per launch
+            per = json.loads(tp.read_text()).get("dram_bytes_per_eval")
+            traffic = None if per is None else round(per * n_cand)
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "peak_kind": peak_kind, "bytes_per_eval": per_eval,
+                "traffic_source": "profiles/k1_traffic.json (ncu dram__bytes_read+write per eval x candidates)",
                 "note": "algorithmic bytes per SURVEY §8(d) (32n+12m+12); only the op stream "
                         "is compulsory HBM traffic, d/p gathers are L2-resident"}
         cpu = None
