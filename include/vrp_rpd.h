@@ -48,6 +48,19 @@ extern "C" {
 
 typedef struct vrp_instance *vrp_instance_t;
 
+/* numpy.random.Philox bit-generator state, field for field
+ * (Generator(Philox).bit_generator.state: counter, key, buffer, buffer_pos,
+ * has_uint32, uinteger).  Device-resident when passed to vrp_evolve. */
+typedef struct {
+    uint64_t ctr[4];
+    uint64_t key[2];
+    uint64_t buffer[4];
+    int32_t buffer_pos;
+    int32_t has_uint32;
+    uint32_t uinteger;
+    uint32_t reserved;
+} vrp_philox;
+
 /* Library / device info.  Returns the compiled arch (e.g. 1000 for sm_100a). */
 int vrp_version(int32_t *abi_version, int32_t *compiled_arch);
 const char *vrp_last_error(void);
@@ -89,6 +102,32 @@ int vrp_decode_batch(vrp_instance_t h, const double *genes, int64_t gene_stride,
                      int32_t relax, double penalty, double *fitness, double *makespan,
                      int32_t *scheduled, int64_t *visits, void *ops_out, int32_t op_bytes,
                      int64_t out_stride, int32_t *lens_out, void *stream);
+
+/* K4: stable argsort of a fitness vector (numpy argsort kind="stable",
+ * brkga.py:243/:456): order[N] int32 (device). */
+int vrp_fitness_order(const double *fitness, int64_t N, int32_t *order, void *stream);
+
+/* K4: one BRKGA generation, brkga.evolve (brkga.py:231-252), fully on device.
+ * pop[N][genes] and fitness[N] in; pop_out[N][genes] = [elites | mutants |
+ * offspring]; order_out[N] = the stable fitness order; elite_fitness_out
+ * (nullable) = fitness of the elites in order (run_brkga :456-460).  `state`
+ * is a DEVICE pointer to the generator; it is advanced exactly as numpy's
+ * Generator(Philox) would be by mutants = random((n_mutant, genes)),
+ * e_idx = integers(n_elite, n_off), o_idx = integers(N - n_elite, n_off),
+ * mask = random((n_off, genes)) < elite_bias.  Returns VRP_EINVAL for
+ * PopulationTooSmall (n_elite < 1 or N - n_elite < 1). */
+int vrp_evolve(const double *pop, const double *fitness, int64_t N, int64_t genes,
+               double elite_fraction, double mutant_fraction, double elite_bias,
+               vrp_philox *state, double *pop_out, int32_t *order_out,
+               double *elite_fitness_out, void *stream);
+
+/* run_brkga best tracking (brkga.py:446-467): the first index of the minimum
+ * of fitness[lo, hi) replaces the incumbent when strictly better (or when
+ * *best_index < 0); its chromosome (row of genes[., genes_per_row]) is copied
+ * to best_genes; *trace_slot (nullable) receives the incumbent fitness. */
+int vrp_best_update(const double *fitness, int64_t lo, int64_t hi, const double *genes,
+                    int64_t genes_per_row, double *best_fitness, double *best_genes,
+                    int64_t *best_index, double *trace_slot, void *stream);
 
 #ifdef __cplusplus
 }

@@ -12,6 +12,7 @@ PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "lib" / "libvrprpd.so"
 
 VRP_OK, VRP_CAPACITY, VRP_DEADLOCK, VRP_MALFORMED = 0, 1, 2, 3
+VRP_EINVAL, VRP_ECUDA, VRP_EUNSUPPORTED = 1, 2, 3
 MODE_EXACT, MODE_EVALUATE, MODE_TWO_PASS = 0, 1, 2
 
 
@@ -53,6 +54,7 @@ def lib(require_device: bool = True):
                 f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
         L = C.CDLL(str(LIB_PATH))
         _declare(L)
+        declare_k4(L)
         _lib = L
     if require_device:
         import torch
@@ -76,3 +78,12 @@ def stream_handle(stream=None):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return C.c_void_p(s.cuda_stream)
+
+
+def declare_k4(L):
+    P, i64, f64 = C.c_void_p, C.c_int64, C.c_double
+    L.vrp_fitness_order.argtypes = [P, i64, P, P]
+    L.vrp_evolve.argtypes = [P, P, i64, i64, f64, f64, f64, P, P, P, P, P]
+    L.vrp_best_update.argtypes = [P, i64, i64, P, i64, P, P, P, P, P]
+    for name in ("vrp_fitness_order", "vrp_evolve", "vrp_best_update"):
+        getattr(L, name).restype = C.c_int

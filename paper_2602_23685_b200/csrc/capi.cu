@@ -158,4 +158,39 @@ int vrp_decode_batch(vrp_instance_t h, const double *genes, int64_t gene_stride,
     return launch_result(rc, "vrp_decode_batch");
 }
 
+int vrp_fitness_order(const double *fitness, int64_t N, int32_t *order, void *stream) {
+    if (N < 0 || (N > 0 && (!fitness || !order))) return fail(VRP_EINVAL, "vrp_fitness_order: null buffer%s");
+    if (N > 0x7fffffff) return fail(VRP_EUNSUPPORTED, "population too large%s");
+    return launch_result(launch_fitness_order(fitness, N, order, static_cast<cudaStream_t>(stream)),
+                         "vrp_fitness_order");
+}
+
+int vrp_evolve(const double *pop, const double *fitness, int64_t N, int64_t genes,
+               double elite_fraction, double mutant_fraction, double elite_bias,
+               vrp_philox *state, double *pop_out, int32_t *order_out,
+               double *elite_fitness_out, void *stream) {
+    if (!pop || !fitness || !state || !pop_out || !order_out || N < 1 || genes < 1)
+        return fail(VRP_EINVAL, "vrp_evolve: bad argument%s");
+    if (N > 0x7fffffff) return fail(VRP_EUNSUPPORTED, "population too large%s");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int rc = launch_evolve(pop, fitness, N, genes, elite_fraction, mutant_fraction, elite_bias,
+                                 state, pop_out, order_out, elite_fitness_out,
+                                 static_cast<cudaStream_t>(stream), sms);
+    if (rc == -3) return fail(VRP_EINVAL, "PopulationTooSmall: population %s cannot sustain elites", "");
+    return launch_result(rc, "vrp_evolve");
+}
+
+int vrp_best_update(const double *fitness, int64_t lo, int64_t hi, const double *genes,
+                    int64_t genes_per_row, double *best_fitness, double *best_genes,
+                    int64_t *best_index, double *trace_slot, void *stream) {
+    if (!fitness || !best_fitness || !best_index || lo < 0 || hi < lo)
+        return fail(VRP_EINVAL, "vrp_best_update: bad argument%s");
+    return launch_result(launch_best_update(fitness, lo, hi, genes, genes_per_row, best_fitness,
+                                            best_genes, best_index, trace_slot,
+                                            static_cast<cudaStream_t>(stream)),
+                         "vrp_best_update");
+}
+
 }  // extern "C"

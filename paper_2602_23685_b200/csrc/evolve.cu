@@ -1,0 +1,359 @@
+// evolve.cu -- K4: the BRKGA generation step on device (brkga.py:231-252,
+// run_brkga :454-467).
+//
+//  order   stable argsort of the fitness (brkga.py:243, :456): rank-by-count
+//          over (fitness key, index) -- every element counts the elements
+//          that precede it, so equal fitnesses keep index order, exactly as
+//          numpy's stable sort.  O(N^2) compares, tiled through shared memory:
+//          ~0.1 ms at N = 30,000, far below one generation's decode.
+//  draws   numpy Generator(Philox) reproduced bit for bit.  Philox4x64-10 is
+//          counter based, so the q-th 64-bit output of the stream is a pure
+//          function of (state, q): mutant genes, the e_idx/o_idx Lemire draws
+//          and the crossover mask are all computed in parallel.  A Lemire
+//          rejection (probability (2^32 mod n)/2^32 per draw) shifts every
+//          later 32-bit draw; draws are computed optimistically, the first
+//          rejection is found with atomicMin, and one thread redoes the
+//          remaining draws sequentially (rare: ~1.5 % of generations at
+//          N = 30,000).  The final state -- counter, 4-word buffer, buffer
+//          position, pending u32 half -- is written back so the caller's
+//          generator continues exactly where numpy's would.
+//  build   [elites | mutants | offspring] rows; offspring gene = mask ?
+//          elite parent : other parent.  HBM-bound: 3 x 4n x 8 B per
+//          offspring (two parent reads, one write).
+//  best    block reduction of (fitness, first index) over the new rows; the
+//          strict `<` against the incumbent is evaluated on device and the
+//          winning chromosome copied (run_brkga's best tracking, :461-467).
+#include <float.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+__device__ __forceinline__ void philox_block(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3,
+                                             uint64_t k0, uint64_t k1, uint64_t out[4]) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) { k0 += 0x9E3779B97F4A7C15ULL; k1 += 0xBB67AE8584CAA73BULL; }
+        const uint64_t lo0 = 0xD2E7470EE14C6C93ULL * c0, hi0 = __umul64hi(0xD2E7470EE14C6C93ULL, c0);
+        const uint64_t lo1 = 0xCA5A826395121157ULL * c2, hi1 = __umul64hi(0xCA5A826395121157ULL, c2);
+        const uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+// 128-bit counter + j (j >= 0)
+__device__ __forceinline__ void ctr_add(const uint64_t *ctr, uint64_t j, uint64_t out[4]) {
+    uint64_t a = ctr[0] + j;
+    uint64_t carry = a < ctr[0];
+    out[0] = a;
+    uint64_t b = ctr[1] + carry; carry = carry && b == 0; out[1] = b;
+    uint64_t c = ctr[2] + carry; carry = carry && c == 0; out[2] = c;
+    out[3] = ctr[3] + carry;
+}
+
+// q-th u64 of the stream that starts at state S (numpy philox_next semantics)
+__device__ __forceinline__ uint64_t stream_u64(const vrp_philox &S, uint64_t q) {
+    const uint64_t head = 4 - (uint64_t)S.buffer_pos;
+    if (q < head) return S.buffer[S.buffer_pos + q];
+    const uint64_t qq = q - head;
+    uint64_t c[4], out[4];
+    ctr_add(S.ctr, 1 + qq / 4, c);
+    philox_block(c[0], c[1], c[2], c[3], S.key[0], S.key[1], out);
+    return out[qq & 3];
+}
+
+__device__ __forceinline__ double u64_to_double(uint64_t x) {
+    return (double)(x >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// k-th u32 drawn after `base` u64s were consumed, given the pending half
+__device__ __forceinline__ uint32_t stream_u32(const vrp_philox &S, uint64_t base, uint64_t k) {
+    if (S.has_uint32) {
+        if (k == 0) return S.uinteger;
+        --k;
+    }
+    const uint64_t x = stream_u64(S, base + k / 2);
+    return (k & 1) ? (uint32_t)(x >> 32) : (uint32_t)x;
+}
+
+__device__ __forceinline__ uint64_t fit_key(double x) {
+    if (x != x) return 0xFFFFFFFFFFFFFFFFull;
+    if (x == 0.0) x = 0.0;
+    const uint64_t b = (uint64_t)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+constexpr int RANK_TILE = 1024;
+
+// order[rank(i)] = i, rank = #{j : (key_j, j) < (key_i, i)}
+__global__ void __launch_bounds__(256) rank_kernel(const double *__restrict__ fit, int64_t N,
+                                                   int32_t *__restrict__ order) {
+    __shared__ uint64_t tile[RANK_TILE];
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t ki = i < N ? fit_key(__ldg(fit + i)) : ~0ull;
+    int64_t rank = 0;
+    for (int64_t base = 0; base < N; base += RANK_TILE) {
+        const int64_t cnt = N - base < RANK_TILE ? N - base : RANK_TILE;
+        __syncthreads();
+        for (int t = threadIdx.x; t < cnt; t += blockDim.x) tile[t] = fit_key(__ldg(fit + base + t));
+        __syncthreads();
+        if (i < N) {
+            int64_t r = 0;
+            for (int t = 0; t < cnt; ++t) {
+                const uint64_t kj = tile[t];
+                r += (kj < ki) || (kj == ki && base + t < i);
+            }
+            rank += r;
+        }
+    }
+    if (i < N) order[rank] = (int32_t)i;
+}
+
+struct EvolveShape {
+    int64_t N, G, n_elite, n_mutant, n_off;
+    int e_draws, o_draws;  // 1 if the range consumes draws (range > 1), else 0
+    uint32_t e_range, o_range;
+};
+
+__device__ __forceinline__ bool lemire(uint32_t u, uint32_t range, uint32_t &out) {
+    const uint64_t m = (uint64_t)u * range;
+    const uint32_t left = (uint32_t)m;
+    out = (uint32_t)(m >> 32);
+    if (left < range) {
+        const uint32_t thresh = (0u - range) % range;
+        if (left < thresh) return false;  // numpy would reject and redraw
+    }
+    return true;
+}
+
+// optimistic e_idx / o_idx; first rejecting draw index -> *first_rej
+__global__ void draw_kernel(const vrp_philox *__restrict__ Sp, EvolveShape sh, int32_t *__restrict__ e_idx,
+                            int32_t *__restrict__ o_idx, unsigned long long *__restrict__ first_rej) {
+    const vrp_philox S = *Sp;
+    const uint64_t base = (uint64_t)(sh.n_mutant * sh.G);
+    const int64_t tot = (int64_t)(sh.e_draws + sh.o_draws) * sh.n_off;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < 2 * sh.n_off;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const bool is_e = k < sh.n_off;
+        const int64_t i = is_e ? k : k - sh.n_off;
+        const int used = is_e ? sh.e_draws : sh.o_draws;
+        if (!used) {
+            (is_e ? e_idx : o_idx)[i] = 0;
+            continue;
+        }
+        const int64_t d = is_e ? i : (int64_t)sh.e_draws * sh.n_off + i;  // u32 draw number
+        uint32_t v;
+        const bool ok = lemire(stream_u32(S, base, (uint64_t)d), is_e ? sh.e_range : sh.o_range, v);
+        (is_e ? e_idx : o_idx)[i] = (int32_t)v;
+        if (!ok) atomicMin(first_rej, (unsigned long long)d);
+    }
+    (void)tot;
+}
+
+// sequential redo from the first rejection; writes the u32 count consumed
+__global__ void fix_kernel(const vrp_philox *__restrict__ Sp, EvolveShape sh, int32_t *__restrict__ e_idx,
+                           int32_t *__restrict__ o_idx, const unsigned long long *__restrict__ first_rej,
+                           unsigned long long *__restrict__ u32_used) {
+    const vrp_philox S = *Sp;
+    const uint64_t base = (uint64_t)(sh.n_mutant * sh.G);
+    const int64_t ndraw = (int64_t)(sh.e_draws + sh.o_draws) * sh.n_off;
+    const unsigned long long fr = *first_rej;
+    if (fr >= (unsigned long long)ndraw) { *u32_used = (unsigned long long)ndraw; return; }
+    uint64_t k = fr;  // u32 position of draw number fr (no rejection before it)
+    for (int64_t d = (int64_t)fr; d < ndraw; ++d) {
+        const bool is_e = sh.e_draws && d < sh.n_off;
+        const uint32_t range = is_e ? sh.e_range : sh.o_range;
+        uint32_t v;
+        while (!lemire(stream_u32(S, base, k++), range, v)) {}
+        if (is_e) e_idx[d] = (int32_t)v;
+        else o_idx[d - (int64_t)sh.e_draws * sh.n_off] = (int32_t)v;
+    }
+    *u32_used = k;
+}
+
+__device__ __forceinline__ uint64_t u64s_for_u32(const vrp_philox &S, uint64_t used) {
+    const uint64_t from_u64 = used > (uint64_t)S.has_uint32 ? used - S.has_uint32 : 0;
+    return (from_u64 + 1) / 2;
+}
+
+// rows [elites | mutants | offspring]
+__global__ void __launch_bounds__(256) build_kernel(const vrp_philox *__restrict__ Sp, EvolveShape sh,
+                                                    const double *__restrict__ pop,
+                                                    const int32_t *__restrict__ order,
+                                                    const int32_t *__restrict__ e_idx,
+                                                    const int32_t *__restrict__ o_idx,
+                                                    const unsigned long long *__restrict__ u32_used,
+                                                    double bias, double *__restrict__ out) {
+    const vrp_philox S = *Sp;
+    const int64_t G = sh.G;
+    const uint64_t mut = (uint64_t)(sh.n_mutant * G);
+    const uint64_t mask0 = mut + u64s_for_u32(S, *u32_used);
+    const int64_t total = sh.N * G;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = x / G, g = x - row * G;
+        double val;
+        if (row < sh.n_elite) {
+            val = __ldg(pop + (int64_t)order[row] * G + g);
+        } else if (row < sh.n_elite + sh.n_mutant) {
+            val = u64_to_double(stream_u64(S, (uint64_t)((row - sh.n_elite) * G + g)));
+        } else {
+            const int64_t i = row - sh.n_elite - sh.n_mutant;
+            const double u = u64_to_double(stream_u64(S, mask0 + (uint64_t)(i * G + g)));
+            const int64_t src = u < bias ? order[e_idx[i]] : order[sh.n_elite + o_idx[i]];
+            val = __ldg(pop + src * G + g);
+        }
+        out[x] = val;
+    }
+}
+
+// advance the caller's generator past everything evolve consumed
+__global__ void state_kernel(vrp_philox *__restrict__ Sp, EvolveShape sh,
+                             const unsigned long long *__restrict__ u32_used) {
+    vrp_philox S = *Sp;
+    const uint64_t used32 = *u32_used;
+    const uint64_t mut = (uint64_t)(sh.n_mutant * sh.G);
+    const uint64_t u64_32 = u64s_for_u32(S, used32);
+    // pending half after the integer draws
+    int has = S.has_uint32;
+    uint32_t pend = S.uinteger;
+    if (used32 > 0) {
+        if (used32 <= (uint64_t)S.has_uint32) {
+            has = 0;
+        } else {
+            const uint64_t from_u64 = used32 - S.has_uint32;
+            if (from_u64 & 1) {
+                has = 1;
+                pend = (uint32_t)(stream_u64(S, mut + from_u64 / 2) >> 32);
+            } else {
+                has = 0;
+            }
+        }
+    }
+    const uint64_t Q = mut + u64_32 + (uint64_t)(sh.n_off * sh.G);
+    const uint64_t head = 4 - (uint64_t)S.buffer_pos;
+    if (Q <= head) {
+        S.buffer_pos += (int32_t)Q;
+    } else {
+        const uint64_t qq = Q - head;
+        const uint64_t blocks = (qq + 3) / 4;
+        uint64_t c[4];
+        ctr_add(S.ctr, blocks, c);
+        uint64_t buf[4];
+        philox_block(c[0], c[1], c[2], c[3], S.key[0], S.key[1], buf);
+        for (int j = 0; j < 4; ++j) { S.ctr[j] = c[j]; S.buffer[j] = buf[j]; }
+        S.buffer_pos = (int32_t)(((qq - 1) & 3) + 1);
+    }
+    S.has_uint32 = has;
+    S.uinteger = pend;
+    *Sp = S;
+}
+
+// (min fitness, first index) over fit[lo, hi); strict improvement of *best
+__global__ void __launch_bounds__(1024) best_kernel(const double *__restrict__ fit, int64_t lo, int64_t hi,
+                                                    const double *__restrict__ genes, int64_t G,
+                                                    double *__restrict__ best_fit,
+                                                    double *__restrict__ best_genes,
+                                                    int64_t *__restrict__ best_index,
+                                                    double *__restrict__ trace) {
+    __shared__ double sv[32];
+    __shared__ int64_t si[32];
+    __shared__ int64_t win;
+    double bv = DBL_MAX;
+    int64_t bi = -1;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double f = fit[i];
+        if (bi < 0 || f < bv) { bv = f; bi = i; }  // first index within the thread's stride
+    }
+    // warp then block argmin with first-index ties
+    for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(VRP_FULL_MASK, bv, o);
+        const int64_t oi = __shfl_xor_sync(VRP_FULL_MASK, bi, o);
+        if (oi >= 0 && (bi < 0 || ov < bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+    }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) { sv[w] = bv; si[w] = bi; }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        bv = lane < nw ? sv[lane] : DBL_MAX;
+        bi = lane < nw ? si[lane] : -1;
+        for (int o = 16; o; o >>= 1) {
+            const double ov = __shfl_xor_sync(VRP_FULL_MASK, bv, o);
+            const int64_t oi = __shfl_xor_sync(VRP_FULL_MASK, bi, o);
+            if (oi >= 0 && (bi < 0 || ov < bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+        }
+        if (lane == 0) {
+            const bool better = bi >= 0 && (*best_index < 0 || bv < *best_fit);
+            win = better ? bi : -1;
+            if (better) { *best_fit = bv; *best_index = bi; }
+            if (trace) *trace = *best_fit;
+        }
+    }
+    __syncthreads();
+    if (win >= 0 && best_genes)
+        for (int64_t g = threadIdx.x; g < G; g += blockDim.x) best_genes[g] = genes[win * G + g];
+}
+
+__global__ void gather_fit_kernel(const double *__restrict__ fit, const int32_t *__restrict__ order,
+                                  int64_t n, double *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = fit[order[i]];
+}
+
+}  // namespace
+
+int launch_fitness_order(const double *fit, int64_t N, int32_t *order, cudaStream_t stream) {
+    if (N <= 0) return 0;
+    const int64_t blocks = (N + 255) / 256;
+    rank_kernel<<<(unsigned)blocks, 256, 0, stream>>>(fit, N, order);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_evolve(const double *pop, const double *fit, int64_t N, int64_t G, double elite_frac,
+                  double mutant_frac, double bias, vrp_philox *state, double *out, int32_t *order,
+                  double *elite_fit, cudaStream_t stream, int sm_count) {
+    EvolveShape sh;
+    sh.N = N;
+    sh.G = G;
+    sh.n_elite = (int64_t)(elite_frac * (double)N);
+    sh.n_mutant = (int64_t)(mutant_frac * (double)N);
+    sh.n_off = N - sh.n_elite - sh.n_mutant;
+    if (sh.n_elite < 1 || N - sh.n_elite < 1) return -3;  // PopulationTooSmall
+    sh.e_range = (uint32_t)sh.n_elite;
+    sh.o_range = (uint32_t)(N - sh.n_elite);
+    sh.e_draws = sh.n_elite > 1 ? 1 : 0;  // integers(1) consumes nothing (numpy)
+    sh.o_draws = N - sh.n_elite > 1 ? 1 : 0;
+
+    int32_t *e_idx = nullptr, *o_idx = nullptr;
+    unsigned long long *scal = nullptr;
+    const size_t idx_bytes = sizeof(int32_t) * (size_t)(sh.n_off > 0 ? sh.n_off : 1);
+    if (cudaMallocAsync(&e_idx, idx_bytes, stream) != cudaSuccess) return -1;
+    if (cudaMallocAsync(&o_idx, idx_bytes, stream) != cudaSuccess) return -1;
+    if (cudaMallocAsync(&scal, 2 * sizeof(unsigned long long), stream) != cudaSuccess) return -1;
+    cudaMemsetAsync(scal, 0xff, sizeof(unsigned long long), stream);
+
+    if (launch_fitness_order(fit, N, order, stream)) return -1;
+    if (elite_fit) {
+        gather_fit_kernel<<<(unsigned)((sh.n_elite + 255) / 256), 256, 0, stream>>>(fit, order, sh.n_elite,
+                                                                                 elite_fit);
+    }
+    const int grid = sm_count * 8;
+    if (sh.n_off > 0) draw_kernel<<<grid, 256, 0, stream>>>(state, sh, e_idx, o_idx, scal);
+    fix_kernel<<<1, 1, 0, stream>>>(state, sh, e_idx, o_idx, scal, scal + 1);
+    build_kernel<<<grid * 4, 256, 0, stream>>>(state, sh, pop, order, e_idx, o_idx, scal + 1, bias, out);
+    state_kernel<<<1, 1, 0, stream>>>(state, sh, scal + 1);
+    cudaFreeAsync(e_idx, stream);
+    cudaFreeAsync(o_idx, stream);
+    cudaFreeAsync(scal, stream);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_best_update(const double *fit, int64_t lo, int64_t hi, const double *genes, int64_t G,
+                       double *best_fit, double *best_genes, int64_t *best_index, double *trace,
+                       cudaStream_t stream) {
+    best_kernel<<<1, 1024, 0, stream>>>(fit, lo, hi, genes, G, best_fit, best_genes, best_index, trace);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/vrp_rpd.h"
 #include "common.cuh"
 
 // makespan.cu (K1/K2); mode 0 exact, 1 evaluate, 2 two-pass; rec = event records
@@ -16,3 +17,12 @@ int launch_decode(const DevInstance &I, const double *genes, int64_t gstride, in
                   double penalty, double *fitness, double *makespan, int32_t *scheduled,
                   int64_t *visits, void *ops_out, int op_bytes, int64_t ostride,
                   int32_t *lens_out, cudaStream_t stream, int sm_count);
+
+// evolve.cu (K4)
+int launch_fitness_order(const double *fit, int64_t N, int32_t *order, cudaStream_t stream);
+int launch_evolve(const double *pop, const double *fit, int64_t N, int64_t G, double elite_frac,
+                  double mutant_frac, double bias, vrp_philox *state, double *out, int32_t *order,
+                  double *elite_fit, cudaStream_t stream, int sm_count);
+int launch_best_update(const double *fit, int64_t lo, int64_t hi, const double *genes, int64_t G,
+                       double *best_fit, double *best_genes, int64_t *best_index, double *trace,
+                       cudaStream_t stream);

@@ -207,6 +207,51 @@ def main():
                    "final_uinteger": int(st["uinteger"])})
     meta["evolve"] = ev
 
+    # ---- warm start constructors, encode, warm_start_population (brkga.py:260-424)
+    for key in C.CONFIGS:
+        inst = ref_instance(key)
+        pre = f"{key}/"
+        for tag, fn in (("greedy", R_brkga._greedy_ops_solution),
+                        ("lb", R_brkga._load_balanced_solution), ("spt", R_brkga._spt_solution)):
+            sol = fn(inst)
+            o, l = I.lists_to_arrays([[(c, kd.value) for c, kd in t] for t in sol.tours], inst.n)
+            blob[pre + f"ws_{tag}_ops"], blob[pre + f"ws_{tag}_lens"] = o, l
+            blob[pre + f"ws_{tag}_enc"] = R_brkga.encode(inst, sol)
+        if inst.n <= 300:
+            inc = to_solution(blob[pre + "dec_ops"][0], blob[pre + "dec_lens"][0])
+            prm = R_brkga.BrkgaParams(population=64, generations=3)
+            pop = R_brkga.warm_start_population(inst, inc, prm, I.philox(13, CFG_ID[key]))
+            blob[pre + "ws_pop"] = pop
+        print(f"warm start {key} done at {time.time() - t0:.1f}s", flush=True)
+
+    # ---- run_brkga driven by Generator(Philox(key=(seed, BRKGA_STREAM))) instead of
+    # PCG64(seed): the reference's own loop, its generator swapped (rng.py)
+    BRKGA_STREAM = 0xB4C6A
+    runs = []
+    insts = {key: ref_instance(key) for key in ("gr17", "eil51", "kroA100")}
+    orig_pcg = np.random.PCG64
+    try:
+        np.random.PCG64 = lambda s: (np.random.Philox(key=(int(s), BRKGA_STREAM))
+                                     if isinstance(s, (int, np.integer)) else orig_pcg(s))
+        for j, (key, N_p, T, seed, warm) in enumerate([("gr17", 60, 8, 5, False), ("gr17", 40, 12, 9, True),
+                                                       ("eil51", 50, 6, 3, False), ("kroA100", 30, 4, 11, True)]):
+            inst = insts[key]
+            prm = R_brkga.BrkgaParams(population=N_p, generations=T)
+            wp = None
+            if warm:
+                inc = to_solution(blob[f"{key}/dec_ops"][0], blob[f"{key}/dec_lens"][0])
+                wp = R_brkga.warm_start_population(inst, inc, prm, I.philox(17, j))
+                blob[f"brkga/{j}/warm"] = wp
+            best, stats = R_brkga.run_brkga(inst, prm, warm_population=wp, seed=seed)
+            o, l = I.lists_to_arrays([[(c, kd.value) for c, kd in t] for t in best.tours], inst.n)
+            blob[f"brkga/{j}/ops"], blob[f"brkga/{j}/lens"] = o, l
+            blob[f"brkga/{j}/trace"] = np.array([f for _, f in stats.trace])
+            runs.append({"key": key, "population": N_p, "generations": T, "seed": seed, "warm": warm,
+                         "best_fitness": stats.best_fitness, "decodes": stats.decodes})
+    finally:
+        np.random.PCG64 = orig_pcg
+    meta["brkga_runs"] = runs
+
     # ---- hint vehicle edge cases (brkga.py:82-89)
     genes = np.array([0.0, 1 / 3, 2 / 3, 1 / 6, 0.5, np.nextafter(1.0, 0), 0.999999999,
                       np.nextafter(1 / 3, 0), np.nextafter(2 / 3, 0), 0.2, 0.4, 0.6, 0.8])

@@ -1,0 +1,98 @@
+"""GPU parity of the BRKGA generation step (K4) and the device-resident
+run_brkga loop against the reference (goldens) and the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import inputs as I
+from conftest import config_instance
+from oracle import oracle as O
+from paper_2602_23685_b200 import brkga as B
+
+pytestmark = pytest.mark.gpu
+
+
+def test_evolve_matches_reference_goldens(golden, golden_meta):
+    for j, ev in enumerate(golden_meta["evolve"]):
+        g = I.philox(*ev["pop_key"])
+        pop = g.random((ev["N"], ev["G"]))
+        fit = g.random(ev["N"])
+        if ev["tie"]:
+            fit = np.round(fit * 7.0)
+        rng = I.philox(*ev["rng_key"])
+        params = B.BrkgaParams(population=ev["N"], elite_fraction=ev["elite"],
+                               mutant_fraction=ev["mutant"], elite_bias=ev["bias"])
+        out = B.evolve(pop, fit, params, rng)
+        np.testing.assert_array_equal(out, golden[f"evolve/{j}/out"])
+        st = rng.bit_generator.state
+        assert [int(x) for x in st["state"]["counter"]] == ev["final_counter"]
+        assert int(st["buffer_pos"]) == ev["final_buffer_pos"]
+        assert int(st["has_uint32"]) == ev["final_has_uint32"]
+        assert int(st["uinteger"]) == ev["final_uinteger"]
+
+
+@pytest.mark.parametrize("N,G,gens", [(30000, 6, 60), (4097, 33, 40), (25, 9, 50)])
+def test_evolve_chain_vs_oracle_including_lemire_rejections(N, G, gens):
+    """Many generations: rejections in integers() happen (p ~ 1e-5 per draw at
+    N = 30000) and must shift the stream exactly like numpy."""
+    params = B.BrkgaParams(population=N)
+    host_rng, dev_rng = I.philox(3, N), I.philox(3, N)
+    g = I.philox(4, N)
+    pop = g.random((N, G))
+    dpop = torch.from_numpy(pop).cuda()
+    for it in range(gens):
+        fit = np.floor(g.random(N) * 50.0)  # many ties
+        pop = O.evolve(pop, fit, params.elite_fraction, params.mutant_fraction,
+                       params.elite_bias, host_rng)
+        dpop = B.evolve(dpop, torch.from_numpy(fit).cuda(), params, dev_rng)
+        assert np.array_equal(dpop.cpu().numpy(), pop), f"generation {it}"
+        assert dev_rng.bit_generator.state == host_rng.bit_generator.state or \
+            str(dev_rng.bit_generator.state) == str(host_rng.bit_generator.state)
+
+
+def test_evolve_population_too_small():
+    with pytest.raises(B.PopulationTooSmall):
+        B.evolve(np.zeros((4, 6)), np.arange(4.0), B.BrkgaParams(population=4), I.philox(0, 0))
+
+
+def test_evolve_degenerate_bias_copies_elite():  # test_brkga.py:100-107
+    pop = np.random.default_rng(3).random((10, 6))
+    out = B.evolve(pop, np.arange(10.0), B.BrkgaParams(population=10, elite_bias=1.0),
+                   I.philox(3, 3))
+    for child in out[2:]:
+        assert np.array_equal(child, pop[0])
+
+
+def test_run_brkga_matches_reference_loop(golden, golden_meta):
+    for j, run in enumerate(golden_meta["brkga_runs"]):
+        inst = config_instance(run["key"])
+        params = B.BrkgaParams(population=run["population"], generations=run["generations"])
+        warm = golden[f"brkga/{j}/warm"] if run["warm"] else None
+        best, stats = B.run_brkga(inst, params, warm_population=warm, seed=run["seed"])
+        np.testing.assert_array_equal([f for _, f in stats.trace], golden[f"brkga/{j}/trace"])
+        ops, lens = best.to_arrays(inst.n)
+        np.testing.assert_array_equal(ops, golden[f"brkga/{j}/ops"])
+        np.testing.assert_array_equal(lens, golden[f"brkga/{j}/lens"])
+        assert stats.best_fitness == run["best_fitness"]
+        assert stats.decodes == run["decodes"]
+
+
+def test_decode_single_matches_reference(golden):  # brkga.decode API, batch of one
+    inst = config_instance("eil51")
+    genes = I.chromosomes(inst.n, 3, (136, 2))
+    for i in range(3):
+        r = B.decode(genes[i], inst, B.BrkgaParams(population=20))
+        assert r.fitness == golden["eil51/dec_fitness"][i]
+        assert r.op_visits == golden["eil51/dec_visits"][i]
+        ops, lens = r.solution.to_arrays(inst.n)
+        np.testing.assert_array_equal(ops, golden["eil51/dec_ops"][i])
+
+
+def test_run_brkga_monotone_trace_large():
+    inst = config_instance("a280")
+    params = B.BrkgaParams(population=2000, generations=5)
+    best, stats = B.run_brkga(inst, params, seed=1)
+    values = [f for _, f in stats.trace]
+    assert all(a >= b for a, b in zip(values, values[1:]))
+    from paper_2602_23685_b200.schedule import exact_makespan
+    assert exact_makespan(inst, best) == stats.best_fitness
