@@ -223,13 +223,11 @@ __global__ void state_kernel(vrp_philox *__restrict__ Sp, EvolveShape sh,
         if (used32 <= (uint64_t)S.has_uint32) {
             has = 0;
         } else {
+            // numpy keeps the high half of the last u64 it split in `uinteger`,
+            // pending (odd count) or already consumed (even count, stale)
             const uint64_t from_u64 = used32 - S.has_uint32;
-            if (from_u64 & 1) {
-                has = 1;
-                pend = (uint32_t)(stream_u64(S, mut + from_u64 / 2) >> 32);
-            } else {
-                has = 0;
-            }
+            has = (int)(from_u64 & 1);
+            pend = (uint32_t)(stream_u64(S, mut + (from_u64 - 1) / 2) >> 32);
         }
     }
     const uint64_t Q = mut + u64_32 + (uint64_t)(sh.n_off * sh.G);
