@@ -45,13 +45,13 @@ class DeviceInstance:
         return self._h
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and N._lib is not None:
-            try:
+        try:
+            h = getattr(self, "_h", None)
+            if h is not None and N._lib is not None:
                 N._lib.vrp_instance_destroy(h)
-            except Exception:  # interpreter shutdown
-                pass
             self._h = None
+        except Exception:  # interpreter shutdown: module globals already gone
+            pass
 
 
 def device_instance(instance) -> DeviceInstance:
