@@ -104,3 +104,33 @@ def test_run_brkga_monotone_trace_large():
     assert all(a >= b for a, b in zip(values, values[1:]))
     from paper_2602_23685_b200.schedule import exact_makespan
     assert exact_makespan(inst, best) == stats.best_fitness
+
+
+@pytest.mark.parametrize("key", [(77, 9), (77, 13), (77, 47)])
+def test_evolve_forced_lemire_rejection(key):
+    """Philox keys found (by a numpy search over the raw stream) to make numpy
+    reject an e_idx (key 9) or o_idx (13, 47) draw in the first generation at
+    N = 30000, G = 6: exercises the sequential fix-up path."""
+    N, G = 30000, 6
+    params = B.BrkgaParams(population=N)
+    g = I.philox(5, 5)
+    pop = g.random((N, G))
+    fit = g.random(N)
+    host_rng, dev_rng = I.philox(*key), I.philox(*key)
+    ref = O.evolve(pop, fit, params.elite_fraction, params.mutant_fraction, params.elite_bias,
+                   host_rng)
+    out = B.evolve(pop, fit, params, dev_rng)
+    np.testing.assert_array_equal(out, ref)
+    assert same_state(dev_rng, host_rng)
+
+
+def test_single_island_equals_run_brkga():
+    """world size 1: the island loop with the device engine is run_brkga."""
+    from paper_2602_23685_b200 import islands as IS
+    inst = config_instance("eil51")
+    params = B.BrkgaParams(population=300, generations=7)
+    genes, st = IS.run_islands(inst, params, IS.IslandParams(), seed=4)
+    best, stats = B.run_brkga(inst, params, seed=4)
+    assert st.global_best == stats.best_fitness
+    res = IS.islands_solution(inst, params, genes)
+    assert res.solution == best

@@ -59,3 +59,21 @@ def test_stable_argsort_matches_numpy():
 def test_evolve_population_too_small():
     with pytest.raises(ValueError):
         O.evolve(np.zeros((4, 6)), np.arange(4.0), 0.15, 0.15, 0.7, I.philox(0, 0))
+
+
+@pytest.mark.parametrize("key", [(77, 9), (77, 13), (77, 47)])
+def test_forced_rejection_keys_really_reject(key):
+    """The keys used by test_gpu_brkga's forced-rejection test do make numpy's
+    integers() redraw: with one rejection the Philox stream is one u32 longer
+    than the rejection-free count."""
+    N, G = 30000, 6
+    ne, nm = int(0.15 * N), int(0.15 * N)
+    no = N - ne - nm
+    g = I.philox(*key)
+    g.random((nm, G))
+    g.integers(ne, size=no)
+    g.integers(N - ne, size=no)
+    st = g.bit_generator.state
+    consumed_u64 = (int(st["state"]["counter"][0]) - 1) * 4 + int(st["buffer_pos"])
+    used32 = 2 * (consumed_u64 - nm * G) - int(st["has_uint32"])
+    assert used32 == 2 * no + 1
