@@ -93,6 +93,12 @@ def lib():
         L.orc_philox_integers.argtypes = [C.POINTER(PhiloxState), C.c_uint64]
         L.orc_philox_integers.restype = C.c_uint64
         L.orc_default_threads.restype = i32
+        L.orc_py_sum.argtypes = [P, C.c_int]
+        L.orc_py_sum.restype = f64
+        L.orc_reinsert_all.argtypes = [i32, i32, i32, P, P, P, P, P, i32, i32, C.POINTER(PhiloxState)]
+        L.orc_reinsert_all.restype = C.c_int
+        L.orc_remove_customers.argtypes = [i32, i32, i32, P, P, P, i32, P]
+        L.orc_remove_customers.restype = C.c_int
         _lib = L
     return _lib
 
@@ -190,3 +196,41 @@ def stable_argsort(x):
 
 def default_threads() -> int:
     return int(lib().orc_default_threads())
+
+
+def remove_customers(inst, ops, lens, customers):
+    """insertion.remove_customers: (ops, lens, removed sorted)."""
+    n, m, k, d, p = _inst(inst)
+    ops = np.array(ops, dtype=np.int32).reshape(-1).copy()
+    full = np.full(max(2 * n, ops.size), -1, np.int32)
+    full[:ops.size] = ops
+    lens = np.array(lens, dtype=np.int32).copy()
+    cust = np.ascontiguousarray(customers, dtype=np.int32)
+    out = np.zeros(n, np.int32)
+    cnt = lib().orc_remove_customers(n, m, k, _ptr(full), _ptr(lens), _ptr(cust), cust.size, _ptr(out))
+    return full, lens, out[:cnt].copy()
+
+
+def reinsert_all(inst, ops, lens, removed, regret_k=0, gen=None):
+    """insertion.reinsert_all on a fresh InsertionContext(partial): returns
+    (status, ops, lens); status 1 = RepairFailed.  ``gen`` (Generator(Philox)
+    or None) is advanced like the reference's rng."""
+    n, m, k, d, p = _inst(inst)
+    full = np.full(2 * n, -1, np.int32)
+    ops = np.asarray(ops, dtype=np.int32).reshape(-1)
+    lens = np.array(lens, dtype=np.int32).copy()
+    full[:int(lens.sum())] = ops[:int(lens.sum())]
+    rem = np.ascontiguousarray(removed, dtype=np.int32)
+    st = None
+    if gen is not None:
+        st = PhiloxState.from_numpy(gen)
+    rc = lib().orc_reinsert_all(n, m, k, _ptr(d), _ptr(p), _ptr(full), _ptr(lens), _ptr(rem),
+                                rem.size, int(regret_k), C.byref(st) if st is not None else None)
+    if gen is not None:
+        gen.bit_generator.state = st.to_numpy_state()
+    return rc, full, lens
+
+
+def py_sum(x):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    return float(lib().orc_py_sum(_ptr(x), x.size))

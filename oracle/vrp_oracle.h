@@ -83,6 +83,14 @@ int orc_evolve(const double *pop, const double *fit, int64_t N, int64_t G,
                double elite_frac, double mutant_frac, double bias, orc_philox *rng,
                double *out);
 
+/* insertion.py restatement (insertion_oracle.c) */
+double orc_py_sum(const double *x, int cnt);
+int orc_reinsert_all(int32_t n, int32_t m, int32_t k, const double *d, const double *p,
+                     int32_t *ops, int32_t *lens, const int32_t *removed, int32_t nremoved,
+                     int32_t regret_k, orc_philox *rng);
+int orc_remove_customers(int32_t n, int32_t m, int32_t k, int32_t *ops, int32_t *lens,
+                         const int32_t *customers, int32_t ncust, int32_t *removed_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -252,6 +252,57 @@ def main():
         np.random.PCG64 = orig_pcg
     meta["brkga_runs"] = runs
 
+    # ---- removal cascade + repair (insertion.py:379-516) and destroy (alns.py:182-251),
+    # the reference driven by Generator(Philox) where it takes an rng
+    from vrp_rpd import alns as R_alns
+    from vrp_rpd import insertion as R_ins
+    repairs, destroys = [], []
+    for key, ncase, q in (("gr17", 12, 4), ("eil51", 12, 5), ("kroA100", 8, 5), ("a280", 4, 8)):
+        inst = ref_instance(key)
+        for j in range(ncase):
+            sol = to_solution(blob[f"{key}/dec_ops"][j], blob[f"{key}/dec_lens"][j])
+            pick = I.philox(31, CFG_ID[key], j).choice(np.arange(1, inst.n + 1), size=q, replace=False)
+            tours, removed = R_ins.remove_customers(inst, sol, [int(x) for x in pick])
+            po, pl = I.lists_to_arrays([[(c, kd.value) for c, kd in t] for t in tours], inst.n)
+            regret_k = (0, 2, 3, inst.m)[j % 4]
+            use_rng = j % 6 != 5
+            rng = I.philox(37, CFG_ID[key], j) if use_rng else None
+            ctx = R_ins.InsertionContext(inst, tours)
+            try:
+                R_ins.reinsert_all(ctx, removed, regret_k=regret_k, rng=rng)
+                st = 0
+                ro, rl = I.lists_to_arrays([[(c, kd.value) for c, kd in t] for t in ctx.tours], inst.n)
+            except R_ins.RepairFailed:
+                st, ro, rl = 1, np.full(2 * inst.n, -1, np.int32), np.zeros(inst.m, np.int32)
+            tag = f"repair/{len(repairs)}"
+            blob[tag + "/pick"] = np.asarray(pick, np.int32)
+            blob[tag + "/partial_ops"], blob[tag + "/partial_lens"] = po, pl
+            blob[tag + "/removed"] = np.asarray(removed, np.int32)
+            blob[tag + "/ops"], blob[tag + "/lens"] = ro, rl
+            rs = rng.bit_generator.state if use_rng else None
+            repairs.append({"key": key, "case": j, "regret_k": regret_k, "rng": use_rng, "status": st,
+                            "final_counter": [int(x) for x in rs["state"]["counter"]] if rs else None,
+                            "final_buffer_pos": int(rs["buffer_pos"]) if rs else None,
+                            "final_has_uint32": int(rs["has_uint32"]) if rs else None,
+                            "final_uinteger": int(rs["uinteger"]) if rs else None})
+        for j, op in enumerate(R_alns.DESTROY_OPERATORS * 2):
+            sol = to_solution(blob[f"{key}/dec_ops"][j], blob[f"{key}/dec_lens"][j])
+            rng = I.philox(41, CFG_ID[key], j)
+            partial, removed = R_alns.destroy(inst, sol, op, q, rng)
+            po, pl = I.lists_to_arrays([[(c, kd.value) for c, kd in t] for t in partial.tours], inst.n)
+            tag = f"destroy/{len(destroys)}"
+            blob[tag + "/ops"], blob[tag + "/lens"] = po, pl
+            blob[tag + "/removed"] = np.asarray(removed, np.int32)
+            rs = rng.bit_generator.state
+            destroys.append({"key": key, "case": j, "operator": op, "q": q,
+                             "final_counter": [int(x) for x in rs["state"]["counter"]],
+                             "final_buffer_pos": int(rs["buffer_pos"]),
+                             "final_has_uint32": int(rs["has_uint32"]),
+                             "final_uinteger": int(rs["uinteger"])})
+        print(f"repair/destroy {key} done at {time.time() - t0:.1f}s", flush=True)
+    meta["repairs"] = repairs
+    meta["destroys"] = destroys
+
     # ---- hint vehicle edge cases (brkga.py:82-89)
     genes = np.array([0.0, 1 / 3, 2 / 3, 1 / 6, 0.5, np.nextafter(1.0, 0), 0.999999999,
                       np.nextafter(1 / 3, 0), np.nextafter(2 / 3, 0), 0.2, 0.4, 0.6, 0.8])
