@@ -129,6 +129,23 @@ int vrp_best_update(const double *fitness, int64_t lo, int64_t hi, const double 
                     int64_t genes_per_row, double *best_fitness, double *best_genes,
                     int64_t *best_index, double *trace_slot, void *stream);
 
+/* K5: ALNS repair, insertion.reinsert_all (insertion.py:484-516) on a fresh
+ * InsertionContext of each partial solution, N independent instances.
+ *   partial_ops[N][partial_stride] int32 + partial_lens[N][m]   (vehicle-major)
+ *   removed[N][removed_stride] int32 customers, nremoved[N]       (any order)
+ *   regret_k[N]: 0 = greedy, k >= 2 = regret-k (alns.py:258/:266)
+ *   states[N]: per-instance numpy-Philox generators (DEVICE), advanced exactly
+ *              as the reference's rng; NULL = deterministic (rng=None)
+ *   out_ops[N][out_stride] (-1 padded), out_lens[N][m]
+ *   status[N]: 0 OK, 1 RepairFailed (some customer has no insertion), 2 malformed input
+ * The repaired solution is NOT re-scored here (the reference's _repair_scored,
+ * alns.py:261-274, follows with exact_makespan: use vrp_makespan_batch). */
+int vrp_repair_batch(vrp_instance_t h, const int32_t *partial_ops, int64_t partial_stride,
+                     const int32_t *partial_lens, const int32_t *removed, int64_t removed_stride,
+                     const int32_t *nremoved, const int32_t *regret_k, vrp_philox *states,
+                     int32_t *out_ops, int64_t out_stride, int32_t *out_lens, int32_t *status,
+                     int64_t N, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

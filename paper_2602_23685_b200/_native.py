@@ -85,5 +85,6 @@ def declare_k4(L):
     L.vrp_fitness_order.argtypes = [P, i64, P, P]
     L.vrp_evolve.argtypes = [P, P, i64, i64, f64, f64, f64, P, P, P, P, P]
     L.vrp_best_update.argtypes = [P, i64, i64, P, i64, P, P, P, P, P]
-    for name in ("vrp_fitness_order", "vrp_evolve", "vrp_best_update"):
+    L.vrp_repair_batch.argtypes = [P, P, i64, P, P, i64, P, P, P, P, i64, P, P, i64, P]
+    for name in ("vrp_fitness_order", "vrp_evolve", "vrp_best_update", "vrp_repair_batch"):
         getattr(L, name).restype = C.c_int

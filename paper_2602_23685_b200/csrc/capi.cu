@@ -193,4 +193,21 @@ int vrp_best_update(const double *fitness, int64_t lo, int64_t hi, const double 
                          "vrp_best_update");
 }
 
+int vrp_repair_batch(vrp_instance_t h, const int32_t *partial_ops, int64_t partial_stride,
+                     const int32_t *partial_lens, const int32_t *removed, int64_t removed_stride,
+                     const int32_t *nremoved, const int32_t *regret_k, vrp_philox *states,
+                     int32_t *out_ops, int64_t out_stride, int32_t *out_lens, int32_t *status,
+                     int64_t N, void *stream) {
+    if (!h) return fail(VRP_EINVAL, "null instance%s");
+    if (N < 0 || (N > 0 && (!partial_ops || !partial_lens || !removed || !nremoved || !regret_k ||
+                            !out_ops || !out_lens || !status)))
+        return fail(VRP_EINVAL, "vrp_repair_batch: null buffer%s");
+    if (out_stride < 2 * (int64_t)h->dev.n) return fail(VRP_EINVAL, "out_stride < 2n%s");
+    if (N == 0) return 0;
+    return launch_result(launch_repair(h->dev, partial_ops, partial_stride, partial_lens, removed,
+                                       removed_stride, nremoved, regret_k, states, out_ops, out_stride,
+                                       out_lens, status, N, static_cast<cudaStream_t>(stream)),
+                         "vrp_repair_batch");
+}
+
 }  // extern "C"

@@ -27,46 +27,9 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "philox.cuh"
 
 namespace {
-
-__device__ __forceinline__ void philox_block(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3,
-                                             uint64_t k0, uint64_t k1, uint64_t out[4]) {
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        if (r) { k0 += 0x9E3779B97F4A7C15ULL; k1 += 0xBB67AE8584CAA73BULL; }
-        const uint64_t lo0 = 0xD2E7470EE14C6C93ULL * c0, hi0 = __umul64hi(0xD2E7470EE14C6C93ULL, c0);
-        const uint64_t lo1 = 0xCA5A826395121157ULL * c2, hi1 = __umul64hi(0xCA5A826395121157ULL, c2);
-        const uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
-        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
-    }
-    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
-}
-
-// 128-bit counter + j (j >= 0)
-__device__ __forceinline__ void ctr_add(const uint64_t *ctr, uint64_t j, uint64_t out[4]) {
-    uint64_t a = ctr[0] + j;
-    uint64_t carry = a < ctr[0];
-    out[0] = a;
-    uint64_t b = ctr[1] + carry; carry = carry && b == 0; out[1] = b;
-    uint64_t c = ctr[2] + carry; carry = carry && c == 0; out[2] = c;
-    out[3] = ctr[3] + carry;
-}
-
-// q-th u64 of the stream that starts at state S (numpy philox_next semantics)
-__device__ __forceinline__ uint64_t stream_u64(const vrp_philox &S, uint64_t q) {
-    const uint64_t head = 4 - (uint64_t)S.buffer_pos;
-    if (q < head) return S.buffer[S.buffer_pos + q];
-    const uint64_t qq = q - head;
-    uint64_t c[4], out[4];
-    ctr_add(S.ctr, 1 + qq / 4, c);
-    philox_block(c[0], c[1], c[2], c[3], S.key[0], S.key[1], out);
-    return out[qq & 3];
-}
-
-__device__ __forceinline__ double u64_to_double(uint64_t x) {
-    return (double)(x >> 11) * (1.0 / 9007199254740992.0);
-}
 
 // k-th u32 drawn after `base` u64s were consumed, given the pending half
 __device__ __forceinline__ uint32_t stream_u32(const vrp_philox &S, uint64_t base, uint64_t k) {

@@ -26,3 +26,10 @@ int launch_evolve(const double *pop, const double *fit, int64_t N, int64_t G, do
 int launch_best_update(const double *fit, int64_t lo, int64_t hi, const double *genes, int64_t G,
                        double *best_fit, double *best_genes, int64_t *best_index, double *trace,
                        cudaStream_t stream);
+
+// repair.cu (K5)
+size_t repair_scratch_bytes(int n, int m);
+int launch_repair(const DevInstance &I, const int32_t *pops, int64_t pstride, const int32_t *plens,
+                  const int32_t *removed, int64_t rstride, const int32_t *nremoved,
+                  const int32_t *regret_k, vrp_philox *states, int32_t *out_ops, int64_t ostride,
+                  int32_t *out_lens, int32_t *status, int64_t N, cudaStream_t stream);

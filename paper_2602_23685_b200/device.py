@@ -232,3 +232,33 @@ def score_host_batch(instance, ops, lens, mode: int = N.MODE_EXACT, chunk: int =
         cur.wait_stream(s)
     cur.synchronize()
     return z.numpy(), status.numpy()
+
+
+def repair_batch(instance, partial_ops, partial_lens, removed, nremoved, regret_k, states=None,
+                 stream=None):
+    """K5: reinsert_all on N partial solutions (device tensors in/out).
+
+    partial_ops [N, >=2n] int32, partial_lens [N, m] int32, removed [N, R] int32
+    (customers), nremoved [N] int32, regret_k [N] int32, states: uint8 [N, 96]
+    device generator states (advanced in place) or None (deterministic).
+    Returns dict(ops [N, 2n], lens [N, m], status [N]) -- status 0 OK,
+    1 RepairFailed, 2 malformed input."""
+    di = device_instance(instance)
+    po = _cuda(partial_ops, torch.int32)
+    pl = _cuda(partial_lens, torch.int32)
+    rm = _cuda(removed, torch.int32)
+    nr = _cuda(nremoved, torch.int32)
+    rk = _cuda(regret_k, torch.int32)
+    Nn = po.shape[0]
+    dev = po.device
+    out = {"ops": torch.empty((Nn, 2 * di.n), dtype=torch.int32, device=dev),
+           "lens": torch.empty((Nn, di.m), dtype=torch.int32, device=dev),
+           "status": torch.empty(Nn, dtype=torch.int32, device=dev)}
+    if states is not None and (states.dtype != torch.uint8 or states.shape[-1] != 96):
+        raise ValueError("states must be uint8 [N, 96] device generator states")
+    N.check(N.lib().vrp_repair_batch(di.handle, N.ptr(po), row_stride(po), N.ptr(pl), N.ptr(rm),
+                                     row_stride(rm) if rm.dim() == 2 else 0, N.ptr(nr), N.ptr(rk),
+                                     N.ptr(states), N.ptr(out["ops"]), 2 * di.n, N.ptr(out["lens"]),
+                                     N.ptr(out["status"]), Nn, N.stream_handle(stream)),
+            "vrp_repair_batch")
+    return out

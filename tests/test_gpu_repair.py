@@ -1,0 +1,88 @@
+"""GPU parity of K5 (ALNS repair, insertion.reinsert_all) against the
+reference's goldens and, at scale, against the oracle -- repaired tours,
+RepairFailed status and the final generator state must all match."""
+import numpy as np
+import pytest
+
+import inputs as I
+from conftest import config_instance
+from oracle import oracle as O
+from paper_2602_23685_b200 import insertion as INS
+
+pytestmark = pytest.mark.gpu
+CID = {"gr17": 1, "eil51": 2, "kroA100": 3, "a280": 4, "dsj1000": 5}
+
+
+def same_state(a, b):
+    sa, sb = a.bit_generator.state, b.bit_generator.state
+    return (np.array_equal(sa["state"]["counter"], sb["state"]["counter"])
+            and np.array_equal(sa["buffer"], sb["buffer"]) and sa["buffer_pos"] == sb["buffer_pos"]
+            and sa["has_uint32"] == sb["has_uint32"] and sa["uinteger"] == sb["uinteger"])
+
+
+def test_repair_matches_reference_goldens(golden, golden_meta):
+    recs = golden_meta["repairs"]
+    by_key = {}
+    for i, rec in enumerate(recs):
+        by_key.setdefault(rec["key"], []).append(i)
+    for key, idx in by_key.items():
+        inst = config_instance(key)
+        ops = np.stack([golden[f"repair/{i}/partial_ops"] for i in idx])
+        lens = np.stack([golden[f"repair/{i}/partial_lens"] for i in idx])
+        removed = [golden[f"repair/{i}/removed"] for i in idx]
+        rks = [recs[i]["regret_k"] for i in idx]
+        with_rng = [i for i in idx if recs[i]["rng"]]
+        without = [i for i in idx if not recs[i]["rng"]]
+        for group, use in ((with_rng, True), (without, False)):
+            if not group:
+                continue
+            sel = [idx.index(i) for i in group]
+            gens = [I.philox(37, CID[key], recs[i]["case"]) for i in group] if use else None
+            o, l, st = INS.reinsert_batch(inst, ops[sel], lens[sel], [removed[j] for j in sel],
+                                          [rks[j] for j in sel], gens)
+            for j, i in enumerate(group):
+                assert st[j] == recs[i]["status"], (key, i)
+                np.testing.assert_array_equal(l[j], golden[f"repair/{i}/lens"], err_msg=f"{key} {i}")
+                np.testing.assert_array_equal(o[j], golden[f"repair/{i}/ops"], err_msg=f"{key} {i}")
+                if use:
+                    s = gens[j].bit_generator.state
+                    assert [int(x) for x in s["state"]["counter"]] == recs[i]["final_counter"]
+                    assert int(s["buffer_pos"]) == recs[i]["final_buffer_pos"]
+                    assert int(s["has_uint32"]) == recs[i]["final_has_uint32"]
+
+
+@pytest.mark.parametrize("key,count,q", [("gr17", 64, 6), ("eil51", 64, 8), ("kroA100", 32, 10),
+                                         ("a280", 8, 14)])
+def test_repair_batch_vs_oracle(key, count, q, golden):
+    inst = config_instance(key)
+    genes = I.chromosomes(inst.n, count, (61, CID[key]))
+    dec = O.decode_batch(inst, genes)
+    parts, plens, removed, rks = [], [], [], []
+    for i in range(count):
+        pick = I.philox(62, CID[key], i).choice(np.arange(1, inst.n + 1), size=q, replace=False)
+        o, l, r = O.remove_customers(inst, dec["ops"][i], dec["lens"][i], pick)
+        parts.append(o[:2 * inst.n])
+        plens.append(l)
+        removed.append(r)
+        rks.append((0, 2, 3, inst.m)[i % 4])
+    parts, plens = np.stack(parts), np.stack(plens)
+    dev_gens = [I.philox(63, CID[key], i) for i in range(count)]
+    o, l, st = INS.reinsert_batch(inst, parts, plens, removed, rks, dev_gens)
+    for i in range(count):
+        g = I.philox(63, CID[key], i)
+        rst, ro, rl = O.reinsert_all(inst, parts[i], plens[i], removed[i], rks[i], g)
+        assert st[i] == rst, i
+        if rst == 0:
+            np.testing.assert_array_equal(l[i], rl)
+            np.testing.assert_array_equal(o[i], ro)
+        assert same_state(dev_gens[i], g), i
+
+
+def test_reinsert_all_api_toy():  # test_alns.py:107-116: the toy rebuilds to 47
+    from paper_2602_23685_b200.instance import FleetConfig, Instance
+    from paper_2602_23685_b200.schedule import evaluate
+    toy = Instance(n=2, d=((0, 10, 12), (10, 0, 5), (12, 5, 0)), p=(0, 20, 20),
+                   fleet=FleetConfig(1, 2), label="toy")
+    ctx = INS.InsertionContext(toy, [[]])
+    INS.reinsert_all(ctx, [1, 2], 0, np.random.Generator(np.random.Philox(key=(1, 1))))
+    assert evaluate(toy, ctx.solution()).makespan == 47
