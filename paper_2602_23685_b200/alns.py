@@ -1,0 +1,682 @@
+"""ALNS with simulated annealing -- drop-in for the reference's ``vrp_rpd.alns``
+(``/root/reference/pkg/src/vrp_rpd/alns.py``).
+
+Where the work goes:
+  repair             K5 (csrc/repair.cu) through insertion.reinsert_batch
+  candidate scoring  K1 exact_makespan / K2 two_pass_estimate (csrc/makespan.cu)
+  local search       pickup_repositioning / cross_agent_relocation candidates
+                     are scored in one K2 batch, the best 10 re-scored in one K1
+                     batch (alns.py:401-487)
+  destroy            host (small next to repair); numpy draws in
+                     the reference's order so one generator drives destroy (host)
+                     and repair (device) exactly like the reference's single rng
+  run_pool           all workers advance in lockstep; each iteration repairs
+                     every worker's candidate in ONE K5 launch and scores them
+                     in ONE K1 launch (the "ALNS candidate batch")
+
+RNG: ``run_alns(seed)`` uses ``Generator(Philox(key=(seed, ALNS_STREAM)))``
+where the reference uses PCG64(seed) (see rng.py); with that substitution the
+trajectory is identical to the reference's (tests/test_gpu_alns.py).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import insertion
+from . import rng as R
+from .insertion import InsertionContext, RepairFailed
+from .schedule import (OpKind, ScheduleError, Solution, evaluate, exact_makespan,
+                       pack_solutions, two_pass_estimate)
+
+_D, _P = OpKind.DROPOFF, OpKind.PICKUP
+
+DESTROY_OPERATORS = ("random", "worst", "shaw", "cluster", "route", "critical_path")
+REPAIR_OPERATORS = ("greedy", "regret2", "regret3", "regretm")
+SHAW_TRAVEL_WEIGHT = 9.0
+SHAW_TIME_WEIGHT = 3.0
+SHAW_AGENT_WEIGHT = 5.0
+WORST_POWER = 6.0
+_REGRET_K = {"greedy": 0, "regret2": 2, "regret3": 3}
+_NEAR_BOTTLENECK = 0.9
+_VERIFY_LIMIT = 10
+
+
+@dataclass
+class AlnsParams:
+    t0: float = 0.30
+    alpha: float = 0.9998
+    reheat_factor: float = 0.50
+    stagnation_threshold: int = 2000
+    weight_interval: int = 100
+    reaction: float = 0.1
+    sigma1: float = 33.0
+    sigma2: float = 9.0
+    sigma3: float = 13.0
+    min_weight: float = 0.1
+    max_iter: int = 20000
+    workers_per_pool: int = 32
+    pickup_reposition_interval: int = 200
+    cross_agent_interval: int = 500
+    best_check_interval: int = 1000
+    pool_sync_interval: int = 100
+
+    def __post_init__(self):
+        if not 0.0 < self.alpha < 1.0:
+            raise ValueError("cooling rate must lie in (0, 1)")
+        if not self.sigma1 > self.sigma3 > self.sigma2 > 0:
+            raise ValueError("scores must satisfy sigma1 > sigma3 > sigma2 > 0")
+        for name in ("weight_interval", "pickup_reposition_interval", "cross_agent_interval",
+                     "best_check_interval", "pool_sync_interval"):
+            if getattr(self, name) < 1:
+                raise ValueError(f"{name} must be >= 1")
+
+
+@dataclass
+class OperatorBank:
+    weights: dict
+    scores: dict
+    attempts: dict
+
+    @classmethod
+    def fresh(cls) -> "OperatorBank":
+        names = DESTROY_OPERATORS + REPAIR_OPERATORS
+        return cls(weights=dict.fromkeys(names, 1.0), scores=dict.fromkeys(names, 0.0),
+                   attempts=dict.fromkeys(names, 0))
+
+
+@dataclass
+class AlnsStats:
+    iterations: int = 0
+    initial_makespan: float = 0.0
+    best_trace: list = field(default_factory=list)
+    weight_rows: list = field(default_factory=list)
+    attempts: dict = field(default_factory=dict)
+    accepted: int = 0
+    rejected_candidates: int = 0
+    reheats: int = 0
+    final_temperature: float = 0.0
+
+
+class EmptySolution(Exception):
+    pass
+
+
+def removal_bounds(n: int) -> tuple:
+    """q_max = max(4, n // 20), q_min = max(4, q_max // 2) (alns.py:102-109)."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    q_max = max(4, n // 20)
+    return max(4, q_max // 2), q_max
+
+
+def sa_accept(z_candidate: float, z_current: float, temperature: float, rng) -> bool:
+    if temperature <= 0:
+        raise ValueError("temperature must be positive")
+    if z_candidate < z_current:
+        return True
+    return rng.random() < math.exp(-(z_candidate - z_current) / temperature)
+
+
+def update_weights(bank: OperatorBank, r: float, min_weight: float = 0.1) -> OperatorBank:
+    for name, w in bank.weights.items():
+        a = bank.attempts[name]
+        avg = bank.scores[name] / a if a else 0.0
+        bank.weights[name] = max(min_weight, (1.0 - r) * w + r * avg)
+        bank.scores[name] = 0.0
+        bank.attempts[name] = 0
+    return bank
+
+
+def roulette_select(names, weights: dict, rng) -> str:
+    total = sum(weights[x] for x in names)
+    x = rng.random() * total
+    acc = 0.0
+    for name in names:
+        acc += weights[name]
+        if x < acc:
+            return name
+    return names[-1]
+
+
+def shaw_relatedness(instance, schedule, ci: int, cj: int) -> float:
+    r = SHAW_TRAVEL_WEIGHT * instance.d[ci][cj]
+    r += SHAW_TIME_WEIGHT * abs(schedule.t_drop[ci] - schedule.t_drop[cj])
+    half = SHAW_AGENT_WEIGHT / 2.0
+    if schedule.drop_vehicle[ci] != schedule.drop_vehicle[cj]:
+        r += half
+    if schedule.pickup_vehicle[ci] != schedule.pickup_vehicle[cj]:
+        r += half
+    return r
+
+
+# --------------------------------------------------------------------------
+# destroy (host)
+# --------------------------------------------------------------------------
+
+def _power_law_pick(items, rng, power: float = WORST_POWER):
+    idx = int(rng.random() ** power * len(items))
+    return items[min(idx, len(items) - 1)]
+
+
+def _sample(items, size: int, rng) -> list:
+    pool = list(items)
+    n = len(pool)
+    for i in range(size):
+        j = i + int(rng.integers(n - i))
+        pool[i], pool[j] = pool[j], pool[i]
+    return pool[:size]
+
+
+def destroy(instance, solution: Solution, operator: str, q: int, rng):
+    """Remove (at least) q customers with one of the six operators
+    (alns.py:182-251); returns (partial Solution, removed list)."""
+    n = instance.n
+    if n == 0 or all(not t for t in solution.tours):
+        raise EmptySolution("nothing to remove")
+    q = min(q, n)
+    customers = list(instance.customers)
+    q_min = min(removal_bounds(n)[0], n)
+    d = instance.d
+    if operator == "random":
+        picked = _sample(customers, q, rng)
+    elif operator == "worst":
+        gains = insertion.removal_gains(instance, solution)
+        ranked = sorted(customers, key=lambda c: (-gains[c], c))
+        picked = []
+        while len(picked) < q:
+            c = _power_law_pick(ranked, rng)
+            ranked.remove(c)
+            picked.append(c)
+    elif operator == "shaw":
+        sched = evaluate(instance, solution)
+        seed_c = customers[int(rng.integers(n))]
+        picked = [seed_c]
+        pool = [c for c in customers if c != seed_c]
+        while len(picked) < q and pool:
+            ref = picked[int(rng.integers(len(picked)))]
+            best = min(pool, key=lambda c: (shaw_relatedness(instance, sched, ref, c), c))
+            pool.remove(best)
+            picked.append(best)
+    elif operator == "cluster":
+        center = customers[int(rng.integers(n))]
+        ranked = sorted((c for c in customers if c != center), key=lambda c: (d[center][c], c))
+        picked = [center] + ranked[:q - 1]
+    elif operator == "route":
+        non_empty = [v for v, t in enumerate(solution.tours) if t]
+        v = non_empty[int(rng.integers(len(non_empty)))]
+        picked = sorted({c for c, _ in solution.tours[v]})
+        if len(picked) < q_min:
+            pool = [c for c in customers if c not in picked]
+            while len(picked) < q_min and pool:
+                best = min(pool, key=lambda c: (min(d[c][x] for x in picked), c))
+                pool.remove(best)
+                picked.append(best)
+    elif operator == "critical_path":
+        sched = evaluate(instance, solution)
+        v = sched.bottleneck()
+        on_route = sorted({c for c, _ in solution.tours[v]})
+        if len(on_route) >= q:
+            picked = _sample(on_route, q, rng)
+        else:
+            picked = list(on_route)
+            if len(picked) < q_min:
+                gains = insertion.removal_gains(instance, solution)
+                pool = sorted((c for c in customers if c not in picked), key=lambda c: (-gains[c], c))
+                picked.extend(pool[:q_min - len(picked)])
+    else:
+        raise ValueError(f"unknown destroy operator {operator!r}")
+    tours, removed = insertion.remove_customers(instance, solution, picked)
+    return Solution.from_lists(tours), removed
+
+
+# --------------------------------------------------------------------------
+# repair (device)
+# --------------------------------------------------------------------------
+
+def _repair_scored(instance, partial: Solution, removed, operator: str, rng):
+    if operator not in REPAIR_OPERATORS:
+        raise ValueError(f"unknown repair operator {operator!r}")
+    if not removed:
+        return partial, exact_makespan(instance, partial)
+    ctx = InsertionContext(instance, partial.tours)
+    insertion.reinsert_all(ctx, removed, regret_k=_REGRET_K.get(operator, instance.m), rng=rng)
+    sol = ctx.solution()
+    try:
+        z = exact_makespan(instance, sol)
+    except ScheduleError as exc:
+        raise RepairFailed(str(exc)) from exc
+    return sol, z
+
+
+def repair(instance, partial: Solution, removed, operator: str, rng) -> Solution:
+    if not removed:
+        return partial
+    return _repair_scored(instance, partial, removed, operator, rng)[0]
+
+
+# --------------------------------------------------------------------------
+# initial solution (host construction + device-scored local search)
+# --------------------------------------------------------------------------
+
+def sweep_order(instance) -> list:
+    d = instance.d
+    cs = list(instance.customers)
+    a = max(cs, key=lambda c: (d[0][c], -c))
+    b = max(cs, key=lambda c: (d[a][c], -c))
+    return sorted(cs, key=lambda c: (d[a][c] - d[b][c], d[0][c], c))
+
+
+def _balance_sectors(instance, sectors) -> list:
+    w = {c: 2.0 * instance.d[0][c] + instance.p[c] for c in instance.customers}
+    sectors = [list(s) for s in sectors]
+    loads = [sum(w[c] for c in s) for s in sectors]
+    mean = sum(loads) / len(loads) if loads else 0.0
+    for _ in range(2 * instance.n):
+        if mean <= 0 or max(abs(x - mean) for x in loads) < 0.10 * mean:
+            break
+        hi = max(range(len(loads)), key=lambda i: loads[i])
+        lo = min(range(len(loads)), key=lambda i: loads[i])
+        if not sectors[hi]:
+            break
+        best_c, best_peak = None, max(loads)
+        for c in sectors[hi]:
+            peak = max(loads[hi] - w[c], loads[lo] + w[c],
+                       *(loads[i] for i in range(len(loads)) if i not in (hi, lo)))
+            if peak < best_peak:
+                best_c, best_peak = c, peak
+        if best_c is None:
+            break
+        sectors[hi].remove(best_c)
+        sectors[lo].append(best_c)
+        loads[hi] -= w[best_c]
+        loads[lo] += w[best_c]
+    return sectors
+
+
+def _route_sector(instance, customers) -> list:
+    from .brkga import _route_group
+    return _route_group(instance, customers)
+
+
+def _flat(tours, n):
+    """Tour lists -> (ops int32 [total], lens int32 [m])."""
+    lens = np.array([len(t) for t in tours], np.int32)
+    ops = np.fromiter((2 * (c - 1) + (kind is _P) for t in tours for c, kind in t),
+                      dtype=np.int32, count=int(lens.sum()))
+    return ops, lens
+
+
+def _score_arrays(instance, cand_ops, cand_lens, mode):
+    """One device batch over candidates given as flat op arrays: K2 (mode 2)
+    or K1 (mode 0).  Returns numpy (z, status)."""
+    from .device import makespan_batch
+    n = instance.n
+    K = len(cand_ops)
+    ops = np.full((K, 2 * n), -1, np.int32)
+    for j, o in enumerate(cand_ops):
+        ops[j, :o.size] = o
+    r = makespan_batch(instance, ops, np.stack(cand_lens), mode=mode)
+    return r["z"].cpu().numpy(), r["status"].cpu().numpy()
+
+
+def _apply_best_verified(instance, tours, candidates, z_cur):
+    """Stable sort by estimate, exact-score the best _VERIFY_LIMIT (one K1
+    batch), keep the strongest strict improvement (alns.py:401-413).
+    candidates: [(est, ops, lens)] in generation order."""
+    candidates.sort(key=lambda c: c[0])
+    top = candidates[:_VERIFY_LIMIT]
+    if not top:
+        return None
+    z, st = _score_arrays(instance, [c[1] for c in top], [c[2] for c in top], 0)
+    best = None
+    for zi, si, (_, o, l) in zip(z, st, top):
+        if si != 0:
+            continue
+        if zi < z_cur - 1e-9 and (best is None or zi < best[0]):
+            best = (float(zi), o, l)
+    if best is None:
+        return None
+    return [list(t) for t in Solution.from_arrays(best[1], best[2]).tours]
+
+
+def _estimate_filter(instance, cand_ops, cand_lens, z):
+    """K2 over all candidates; keep (est, ops, lens) with est < z - 1e-9 in
+    generation order (two_pass_estimate errors are skipped)."""
+    if not cand_ops:
+        return []
+    est, st = _score_arrays(instance, cand_ops, cand_lens, 2)
+    return [(float(e), o, l) for e, s, o, l in zip(est, st, cand_ops, cand_lens)
+            if s == 0 and e < z - 1e-9]
+
+
+def pickup_repositioning(instance, solution: Solution) -> Solution:
+    """Move pickups off (near-)bottleneck vehicles; <= 3 improvement passes
+    (alns.py:416-450).  Candidates are built as flat op arrays, estimated in
+    one K2 launch, the best ten verified in one K1 launch."""
+    tours = [list(t) for t in solution.tours]
+    m = instance.m
+    for _ in range(3):
+        sched = evaluate(instance, Solution.from_lists(tours))
+        z = sched.makespan
+        if z <= 0:
+            break
+        hot = sorted({v for v, r in enumerate(sched.returns) if r >= _NEAR_BOTTLENECK * z})
+        ops, lens = _flat(tours, instance.n)
+        starts = np.concatenate([[0], np.cumsum(lens)[:-1]])
+        c_ops, c_lens = [], []
+        for v in hot:
+            for i in range(int(lens[v])):
+                op = int(ops[starts[v] + i])
+                if not op & 1:
+                    continue
+                base = np.delete(ops, starts[v] + i)
+                blens = lens.copy()
+                blens[v] -= 1
+                bstarts = np.concatenate([[0], np.cumsum(blens)[:-1]])
+                for w in range(m):
+                    for g in range(int(blens[w]) + 1):
+                        if w == v and g == i:
+                            continue
+                        cl = blens.copy()
+                        cl[w] += 1
+                        c_ops.append(np.insert(base, bstarts[w] + g, op))
+                        c_lens.append(cl)
+        new_tours = _apply_best_verified(instance, tours, _estimate_filter(instance, c_ops, c_lens, z), z)
+        if new_tours is None:
+            break
+        tours = new_tours
+    return Solution.from_lists(tours)
+
+
+def cross_agent_relocation(instance, solution: Solution) -> Solution:
+    """Move whole customers off the bottleneck route; <= 3 passes (alns.py:453-487)."""
+    if instance.m == 1:
+        return solution
+    tours = [list(t) for t in solution.tours]
+    m = instance.m
+    for _ in range(3):
+        sched = evaluate(instance, Solution.from_lists(tours))
+        z = sched.makespan
+        b = sched.bottleneck()
+        ops, lens = _flat(tours, instance.n)
+        c_ops, c_lens = [], []
+        for c in sorted({c for c, _ in tours[b]}):
+            keep = (ops >> 1) + 1 != c
+            stripped = ops[keep]
+            slens = lens.copy()
+            at = 0
+            for v in range(m):
+                slens[v] = int(keep[at:at + lens[v]].sum())
+                at += int(lens[v])
+            sstarts = np.concatenate([[0], np.cumsum(slens)[:-1]])
+            d_op, p_op = 2 * (c - 1), 2 * (c - 1) + 1
+            for w in range(m):
+                if w == b:
+                    continue
+                L = int(slens[w])
+                cl = slens.copy()
+                cl[w] += 2
+                for gd in range(L + 1):
+                    with_d = np.insert(stripped, sstarts[w] + gd, d_op)
+                    for gp in range(gd + 1, L + 2):
+                        c_ops.append(np.insert(with_d, sstarts[w] + gp, p_op))
+                        c_lens.append(cl)
+        new_tours = _apply_best_verified(instance, tours, _estimate_filter(instance, c_ops, c_lens, z), z)
+        if new_tours is None:
+            break
+        tours = new_tours
+    return Solution.from_lists(tours)
+
+
+def construct_initial(instance, seed: int = 0) -> Solution:
+    """Sweep sectors, balance, greedy-route each, then the local-search pair
+    until no improvement (alns.py:369-390)."""
+    m, n = instance.m, instance.n
+    order = sweep_order(instance)
+    sizes = [n // m + (1 if i < n % m else 0) for i in range(m)]
+    sectors, at = [], 0
+    for s in sizes:
+        sectors.append(order[at:at + s])
+        at += s
+    sectors = _balance_sectors(instance, sectors)
+    sol = Solution.from_lists([_route_sector(instance, sec) for sec in sectors])
+    evaluate(instance, sol)
+    for _ in range(10):
+        z = evaluate(instance, sol).makespan
+        sol = pickup_repositioning(instance, sol)
+        sol = cross_agent_relocation(instance, sol)
+        if evaluate(instance, sol).makespan >= z - 1e-9:
+            break
+    return sol
+
+
+# --------------------------------------------------------------------------
+# main loop
+# --------------------------------------------------------------------------
+
+def _rng_for(seed: int):
+    return R.philox_generator(seed, R.ALNS_STREAM)
+
+
+def worker_seed(seed: int, worker: int) -> int:
+    return int(np.random.SeedSequence([seed, worker]).generate_state(1)[0])
+
+
+class _PoolShare:
+    """Best incumbent shared inside a pool (lockstep pool: no locks needed)."""
+
+    def __init__(self):
+        self.best_z = math.inf
+        self.best_sol = None
+        self.src = None
+
+    def offer(self, worker: int, z: float, sol: Solution) -> None:
+        if z < self.best_z:
+            self.best_z, self.best_sol, self.src = z, sol, worker
+
+    def poll(self, worker: int):
+        if self.best_sol is not None and self.src != worker:
+            return self.best_z, self.best_sol
+        return None
+
+    def merge(self, other: "_PoolShare") -> None:
+        mine = (self.best_z, self.best_sol, self.src)
+        theirs = (other.best_z, other.best_sol, other.src)
+        if mine[0] < theirs[0]:
+            other.best_z, other.best_sol, other.src = mine[0], mine[1], None
+        if theirs[0] < mine[0] and theirs[0] < self.best_z:
+            self.best_z, self.best_sol, self.src = theirs[0], theirs[1], None
+
+
+class _Worker:
+    """One ALNS trajectory (alns.py:536-640) split into phases so that many
+    workers can share the device launches of an iteration."""
+
+    def __init__(self, instance, params: AlnsParams, seed: int, initial=None, share=None,
+                 global_share=None, worker_id: int = 0, rng=None):
+        self.instance, self.params = instance, params
+        self.rng = rng if rng is not None else _rng_for(seed)
+        self.current = initial if initial is not None else construct_initial(instance, seed)
+        self.z = exact_makespan(instance, self.current)
+        self.best, self.z_best = self.current, self.z
+        self.temperature = params.t0 * self.z
+        self.t_init = self.temperature
+        self.bank = OperatorBank.fresh()
+        self.stagnation = 0
+        q_min, q_max = removal_bounds(instance.n)
+        q_min, q_max = min(q_min, instance.n), min(q_max, instance.n)
+        self.stats = AlnsStats(initial_makespan=self.z)
+        self.stats.best_trace.append((0, self.z_best))
+        self.q_draws = (self.rng.integers(q_min, q_max + 1, size=params.max_iter)
+                        if params.max_iter else [])
+        self.share, self.global_share, self.worker_id = share, global_share, worker_id
+
+    def _found_best(self, sol, value, it):
+        self.best, self.z_best = sol, value
+        self.stagnation = 0
+        self.stats.best_trace.append((it, value))
+        if self.share is not None:
+            self.share.offer(self.worker_id, value, sol)
+
+    # phase 1: operator selection + destroy (host)
+    def propose(self, it: int):
+        bank, rng = self.bank, self.rng
+        self.dname = roulette_select(DESTROY_OPERATORS, bank.weights, rng)
+        self.rname = roulette_select(REPAIR_OPERATORS, bank.weights, rng)
+        bank.attempts[self.dname] += 1
+        bank.attempts[self.rname] += 1
+        q = int(self.q_draws[it - 1])
+        try:
+            self.partial, self.removed = destroy(self.instance, self.current, self.dname, q, rng)
+            self.failed = False
+        except (RepairFailed, ScheduleError):
+            self.failed = True
+        if self.rname not in REPAIR_OPERATORS:
+            raise ValueError(f"unknown repair operator {self.rname!r}")
+        return not self.failed
+
+    # phase 3: acceptance + bookkeeping (host), given the repaired candidate
+    def conclude(self, it: int, cand, z_cand, failed: bool):
+        p, bank = self.params, self.bank
+        if failed:
+            self.stats.rejected_candidates += 1
+        elif z_cand < self.z:
+            self.current, self.z = cand, z_cand
+            bank.scores[self.dname] += p.sigma2
+            bank.scores[self.rname] += p.sigma2
+            self.stats.accepted += 1
+            if z_cand < self.z_best:
+                bank.scores[self.dname] += p.sigma1 - p.sigma2
+                bank.scores[self.rname] += p.sigma1 - p.sigma2
+                self._found_best(cand, z_cand, it)
+        elif self.temperature > 0 and self.rng.random() < math.exp(-(z_cand - self.z) / self.temperature):
+            self.current, self.z = cand, z_cand
+            bank.scores[self.dname] += p.sigma3
+            bank.scores[self.rname] += p.sigma3
+            self.stats.accepted += 1
+        self.temperature *= p.alpha
+        self.stagnation += 1
+        if self.stagnation >= p.stagnation_threshold and self.temperature < 0.01 * self.t_init:
+            self.temperature = p.reheat_factor * p.t0 * self.z_best
+            self.stagnation = 0
+            self.stats.reheats += 1
+        if it % p.weight_interval == 0:
+            update_weights(bank, p.reaction, p.min_weight)
+            self.stats.weight_rows.append({"iteration": it, "best_makespan": self.z_best,
+                                           "temperature": self.temperature,
+                                           **{f"w_{k}": bank.weights[k] for k in bank.weights}})
+        inst = self.instance
+        if it % p.pickup_reposition_interval == 0:
+            improved = pickup_repositioning(inst, self.current)
+            z_new = exact_makespan(inst, improved)
+            if z_new < self.z:
+                self.current, self.z = improved, z_new
+                if z_new < self.z_best:
+                    self._found_best(improved, z_new, it)
+        if it % p.cross_agent_interval == 0:
+            improved = cross_agent_relocation(inst, self.current)
+            z_new = exact_makespan(inst, improved)
+            if z_new < self.z:
+                self.current, self.z = improved, z_new
+                if z_new < self.z_best:
+                    self._found_best(improved, z_new, it)
+        if self.share is not None and it % p.best_check_interval == 0:
+            got = self.share.poll(self.worker_id)
+            if got is not None and got[0] < self.z:
+                self.z, self.current = got[0], got[1]
+                if self.z < self.z_best:
+                    self.best, self.z_best = self.current, self.z
+                    self.stats.best_trace.append((it, self.z))
+        if self.share is not None and self.global_share is not None and it % p.pool_sync_interval == 0:
+            self.share.merge(self.global_share)
+
+    def finish(self):
+        self.stats.iterations = self.params.max_iter
+        self.stats.attempts = dict(self.bank.attempts)
+        self.stats.final_temperature = self.temperature
+        return self.best, self.stats
+
+
+def _repair_many(instance, workers):
+    """Repair every live worker's partial in one K5 launch, score in one K1
+    launch; returns [(cand, z, failed)] aligned with ``workers``."""
+    from .device import makespan_batch
+    live = [w for w in workers if not w.failed]
+    out = {id(w): (None, 0.0, True) for w in workers}
+    need = [w for w in live if w.removed]
+    for w in live:
+        if not w.removed:  # nothing removed: the partial is the candidate
+            try:
+                out[id(w)] = (w.partial, exact_makespan(instance, w.partial), False)
+            except ScheduleError:
+                out[id(w)] = (None, 0.0, True)
+    if need:
+        parts, lens = pack_solutions(instance, [w.partial for w in need])
+        o, l, st = insertion.reinsert_batch(
+            instance, parts, lens, [w.removed for w in need],
+            [_REGRET_K.get(w.rname, instance.m) for w in need], [w.rng for w in need])
+        ok = np.flatnonzero(st == 0)
+        if ok.size:
+            r = makespan_batch(instance, o[ok], l[ok], mode=0)
+            z = r["z"].cpu().numpy()
+            zs = r["status"].cpu().numpy()
+        for j, w in enumerate(need):
+            if st[j] != 0:
+                continue
+            k = int(np.searchsorted(ok, j))
+            if zs[k] != 0:
+                continue
+            out[id(w)] = (Solution.from_arrays(o[j], l[j]), float(z[k]), False)
+    return [out[id(w)] for w in workers]
+
+
+def run_alns(instance, params: AlnsParams, seed: int, initial: Solution | None = None,
+             share: _PoolShare | None = None, global_share: _PoolShare | None = None,
+             worker_id: int = 0, rng=None):
+    """Single trajectory (alns.py:536-640); returns (best Solution, AlnsStats)."""
+    w = _Worker(instance, params, seed, initial, share, global_share, worker_id, rng=rng)
+    for it in range(1, params.max_iter + 1):
+        w.propose(it)
+        (cand, z, failed), = _repair_many(instance, [w])
+        w.conclude(it, cand, z, failed)
+    return w.finish()
+
+
+def run_pool(instance, params: AlnsParams, pool_size: int, seed: int,
+             initial: Solution | None = None):
+    """pool_size workers with derived seeds (alns.py:643-685), advanced in
+    lockstep so each iteration is one batched repair + one batched scoring.
+    Workers offer/poll their pool's incumbent in worker order (deterministic;
+    the reference's threads interleave nondeterministically)."""
+    if pool_size < 1:
+        raise ValueError("pool_size must be >= 1")
+    if pool_size == 1:
+        best, stats = run_alns(instance, params, worker_seed(seed, 0), initial=initial)
+        return best, {"workers": 1, "pools": 1, "best_makespan": evaluate(instance, best).makespan,
+                      "worker_stats": [stats]}
+    n_pools = (pool_size + params.workers_per_pool - 1) // params.workers_per_pool
+    pools = [_PoolShare() for _ in range(n_pools)]
+    global_share = _PoolShare() if n_pools > 1 else None
+    workers = [_Worker(instance, params, worker_seed(seed, i), initial,
+                       pools[i // params.workers_per_pool], global_share, i)
+               for i in range(pool_size)]
+    for it in range(1, params.max_iter + 1):
+        for w in workers:
+            w.propose(it)
+        results = _repair_many(instance, workers)
+        for w, (cand, z, failed) in zip(workers, results):
+            w.conclude(it, cand, z, failed)
+    results = [w.finish() for w in workers]
+    best, z_best = None, math.inf
+    for sol, _ in results:
+        z = evaluate(instance, sol).makespan
+        if z < z_best:
+            best, z_best = sol, z
+    for pool in pools:
+        if pool.best_sol is not None and pool.best_z < z_best:
+            best, z_best = pool.best_sol, pool.best_z
+    return best, {"workers": pool_size, "pools": n_pools, "best_makespan": z_best,
+                  "worker_stats": [st for _, st in results]}

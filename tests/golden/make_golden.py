@@ -303,6 +303,46 @@ def main():
     meta["repairs"] = repairs
     meta["destroys"] = destroys
 
+    # ---- construction + local search (alns.py:290-487) and whole ALNS runs
+    # (alns.py:536-640) with _rng_for swapped to Generator(Philox(key=(seed, ALNS_STREAM)))
+    ALNS_STREAM = 0xA1B5
+    for key in ("gr17", "eil51", "kroA100"):
+        inst = ref_instance(key)
+        sol = R_alns.construct_initial(inst, seed=0)
+        o, l = I.lists_to_arrays([[(c, kd.value) for c, kd in t] for t in sol.tours], inst.n)
+        blob[f"ci/{key}/ops"], blob[f"ci/{key}/lens"] = o, l
+        for j in range(3):
+            base = to_solution(blob[f"{key}/dec_ops"][j], blob[f"{key}/dec_lens"][j])
+            for tag, fn in (("pr", R_alns.pickup_repositioning), ("ca", R_alns.cross_agent_relocation)):
+                out = fn(inst, base)
+                o, l = I.lists_to_arrays([[(c, kd.value) for c, kd in t] for t in out.tours], inst.n)
+                blob[f"ls/{key}/{tag}/{j}/ops"], blob[f"ls/{key}/{tag}/{j}/lens"] = o, l
+        print(f"construct/LS {key} done at {time.time() - t0:.1f}s", flush=True)
+    orig_rng_for = R_alns._rng_for
+    runs = []
+    try:
+        R_alns._rng_for = lambda seed: np.random.Generator(np.random.Philox(key=(int(seed), ALNS_STREAM)))
+        for j, (key, iters, seed, init, extra) in enumerate([
+                ("gr17", 60, 3, None, {}), ("gr17", 240, 7, None, {"weight_interval": 50}),
+                ("eil51", 30, 5, None, {}), ("kroA100", 8, 2, "dec", {}),
+                ("eil51", 25, 9, "dec", {"stagnation_threshold": 5, "t0": 0.001})]):
+            inst = ref_instance(key)
+            prm = R_alns.AlnsParams(max_iter=iters, **extra)
+            initial = to_solution(blob[f"{key}/dec_ops"][0], blob[f"{key}/dec_lens"][0]) if init else None
+            best, st = R_alns.run_alns(inst, prm, seed=seed, initial=initial)
+            o, l = I.lists_to_arrays([[(c, kd.value) for c, kd in t] for t in best.tours], inst.n)
+            blob[f"alns/{j}/ops"], blob[f"alns/{j}/lens"] = o, l
+            runs.append({"key": key, "iters": iters, "seed": seed, "init": init, "extra": extra,
+                         "best_trace": st.best_trace, "accepted": st.accepted,
+                         "rejected": st.rejected_candidates, "reheats": st.reheats,
+                         "final_temperature": st.final_temperature, "attempts": st.attempts,
+                         "initial_makespan": st.initial_makespan,
+                         "weight_rows": st.weight_rows})
+            print(f"alns run {j} done at {time.time() - t0:.1f}s", flush=True)
+    finally:
+        R_alns._rng_for = orig_rng_for
+    meta["alns_runs"] = runs
+
     # ---- hint vehicle edge cases (brkga.py:82-89)
     genes = np.array([0.0, 1 / 3, 2 / 3, 1 / 6, 0.5, np.nextafter(1.0, 0), 0.999999999,
                       np.nextafter(1 / 3, 0), np.nextafter(2 / 3, 0), 0.2, 0.4, 0.6, 0.8])
