@@ -343,6 +343,27 @@ def main():
         R_alns._rng_for = orig_rng_for
     meta["alns_runs"] = runs
 
+    # ---- run_pipeline (bench.py:204-222), every PCG64 stream -> Philox
+    from vrp_rpd import bench as R_bench
+    pipes = []
+    orig_pcg = np.random.PCG64
+    try:
+        R_alns._rng_for = lambda seed: np.random.Generator(np.random.Philox(key=(int(seed), ALNS_STREAM)))
+        np.random.PCG64 = lambda s: (np.random.Philox(key=(int(s), BRKGA_STREAM))
+                                     if isinstance(s, (int, np.integer)) else orig_pcg(s))
+        for j, (key, iters, N_p, T, seed) in enumerate([("gr17", 40, 60, 5, 4), ("eil51", 12, 40, 3, 6)]):
+            inst = insts.get(key) or ref_instance(key)
+            sol, inc = R_bench.run_pipeline(inst, R_alns.AlnsParams(max_iter=iters),
+                                            R_brkga.BrkgaParams(population=N_p, generations=T), seed)
+            for tag, x in (("sol", sol), ("inc", inc)):
+                o, l = I.lists_to_arrays([[(c, kd.value) for c, kd in t] for t in x.tours], inst.n)
+                blob[f"pipe/{j}/{tag}_ops"], blob[f"pipe/{j}/{tag}_lens"] = o, l
+            pipes.append({"key": key, "iters": iters, "population": N_p, "generations": T, "seed": seed})
+    finally:
+        R_alns._rng_for = orig_rng_for
+        np.random.PCG64 = orig_pcg
+    meta["pipelines"] = pipes
+
     # ---- hint vehicle edge cases (brkga.py:82-89)
     genes = np.array([0.0, 1 / 3, 2 / 3, 1 / 6, 0.5, np.nextafter(1.0, 0), 0.999999999,
                       np.nextafter(1 / 3, 0), np.nextafter(2 / 3, 0), 0.2, 0.4, 0.6, 0.8])

@@ -71,3 +71,26 @@ def test_run_pool_lockstep_batch():
     one, _ = A.run_pool(inst, A.AlnsParams(max_iter=10), pool_size=1, seed=13, initial=initial)
     direct, _ = A.run_alns(inst, A.AlnsParams(max_iter=10), seed=A.worker_seed(13, 0), initial=initial)
     assert one == direct
+
+
+def test_run_pipeline_matches_reference(golden, golden_meta):
+    from paper_2602_23685_b200 import brkga as B
+    from paper_2602_23685_b200.pipeline import run_pipeline
+    for j, rec in enumerate(golden_meta["pipelines"]):
+        inst = config_instance(rec["key"])
+        sol, inc = run_pipeline(inst, A.AlnsParams(max_iter=rec["iters"]),
+                                B.BrkgaParams(population=rec["population"], generations=rec["generations"]),
+                                rec["seed"])
+        for tag, x in (("sol", sol), ("inc", inc)):
+            ops, lens = x.to_arrays(inst.n)
+            np.testing.assert_array_equal(ops, golden[f"pipe/{j}/{tag}_ops"], err_msg=f"{j} {tag}")
+            np.testing.assert_array_equal(lens, golden[f"pipe/{j}/{tag}_lens"])
+
+
+def test_pipeline_budget_runs():
+    from paper_2602_23685_b200.pipeline import run_pipeline_budget
+    from paper_2602_23685_b200.schedule import evaluate
+    inst = config_instance("gr17")
+    sol, z, trace = run_pipeline_budget(inst, seconds=3.0, pool_size=8)
+    assert evaluate(inst, sol).makespan == z
+    assert all(a[1] >= b[1] for a, b in zip(trace, trace[1:]))
