@@ -140,6 +140,49 @@ def make_candidates(inst, count: int, seed: int, device, chunk: int = 1 << 16):
     return ops, lens, z
 
 
+def extra_rates(device, ops, lens, decode_ms, n_dec):
+    """Secondary §8 throughputs on this GPU (not the headline): K3 decodes/s
+    (the bench set-up, CUDA-event timed), BRKGA generations/s at paper scale
+    (N_p = 30,000) on the a280 island config and dsj1000, ALNS repairs/s
+    (K5, 1024 instances) on the eil51 ALNS config."""
+    import torch
+    from oracle import oracle as O
+    import inputs as I
+    from paper_2602_23685_b200 import brkga as B
+    from paper_2602_23685_b200 import insertion as INS
+    from paper_2602_23685_b200.configs import config_instance
+    out = {"decodes_per_s_dsj1000_random": n_dec / (decode_ms / 1e3)}
+    for key in ("a280", "dsj1000"):
+        inst = config_instance(key)
+        params = B.BrkgaParams(population=30000, generations=1)
+        B.run_brkga(inst, params, seed=0)  # warm
+        params = B.BrkgaParams(population=30000, generations=4)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, st = B.run_brkga(inst, params, seed=1)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        out[f"brkga_generations_per_s_{key}_Np30000"] = 4 / el
+    inst = config_instance("eil51")
+    cnt = 1024
+    genes = I.chromosomes(inst.n, cnt, (7, 7))
+    dec = O.decode_batch(inst, genes)
+    parts, plens, rem = [], [], []
+    for i in range(cnt):
+        pick = I.philox(8, i).choice(np.arange(1, inst.n + 1), size=5, replace=False)
+        o, l, r = O.remove_customers(inst, dec["ops"][i], dec["lens"][i], pick)
+        parts.append(o[:2 * inst.n]); plens.append(l); rem.append(r)
+    parts, plens = np.stack(parts), np.stack(plens)
+    rks = [(0, 2, 3, inst.m)[i % 4] for i in range(cnt)]
+    INS.reinsert_batch(inst, parts[:64], plens[:64], rem[:64], rks[:64], [I.philox(9, i) for i in range(64)])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    INS.reinsert_batch(inst, parts, plens, rem, rks, [I.philox(9, i) for i in range(cnt)])
+    torch.cuda.synchronize()
+    out["alns_repairs_per_s_eil51"] = cnt / (time.perf_counter() - t0)
+    return {k: round(v, 2) for k, v in out.items()}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -190,8 +233,12 @@ def run_gpu(args):
     n_cand = args.candidates
 
     t_setup = time.perf_counter()
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record()
     ops, lens, z_dec = make_candidates(inst, n_cand, seed=1000 + rank, device=dev)
+    d1.record()
     torch.cuda.synchronize()
+    decode_ms = d0.elapsed_time(d1)
     setup_s = time.perf_counter() - t_setup
 
     stream = torch.cuda.current_stream()
@@ -301,6 +348,8 @@ def run_gpu(args):
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": args.steps, "clocks": clk.summary(),
                 "setup_s": round(setup_s, 2)}
+        if not args.no_extra and world == 1:
+            line["extra"] = extra_rates(dev, ops, lens, decode_ms, n_cand)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -318,6 +367,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
