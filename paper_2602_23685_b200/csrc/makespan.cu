@@ -37,6 +37,8 @@ namespace {
 
 constexpr int MODE_EXACT = 0, MODE_EVAL = 1, MODE_TWO = 2;
 constexpr int ST_OK = 0, ST_CAP = 1, ST_DEAD = 2, ST_MAL = 3;
+constexpr int ST_RETRY = 4;                 // internal: narrow ready table overflowed
+constexpr uint32_t NOT_READY32 = 0xFFFFFFFFu;
 constexpr int OPS_AHEAD = 8;   // op codes in registers (positions i .. i+7)
 constexpr int LEGS_AHEAD = 4;  // gathered legs in registers (positions i .. i+3)
 
@@ -48,10 +50,10 @@ struct CandLayout {
     size_t ready, bits, posd, total;
 };
 
-__host__ __device__ inline CandLayout cand_layout(int n, int mode) {
+__host__ __device__ inline CandLayout cand_layout(int n, int mode, int ready_bytes = 8) {
     CandLayout L;
     size_t o = 0;
-    L.ready = o; o += align16(sizeof(double) * (size_t)(n + 1));
+    L.ready = o; o += align16((size_t)ready_bytes * (size_t)(n + 1));
     L.bits = o;  if (mode != MODE_EXACT) o += align16(sizeof(uint32_t) * (size_t)((2 * n + 31) / 32));
     L.posd = o;  if (mode == MODE_TWO) o += align16(sizeof(uint32_t) * (size_t)(n + 1));
     L.total = o;
@@ -137,20 +139,26 @@ struct RouteStream {
     __device__ __forceinline__ int checked_at(int pos) { return checked(fetch(pos), pos); }
 };
 
-template <typename OpT, bool INTD, int MODE, bool REC>
+// NARROW (integral instances, exact/evaluate): the ready table stores uint32
+// (NOT_READY32 = not yet dropped) -- half the shared memory per candidate,
+// twice the resident candidates.  Times are still computed in int64; a value
+// that does not fit marks the candidate ST_RETRY and the launcher re-runs just
+// those candidates with the 64-bit table (`fixup`), so results stay exact.
+template <typename OpT, bool INTD, int MODE, bool REC, bool NARROW>
 __global__ void __launch_bounds__(256)
 makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 const int32_t *__restrict__ lens, int64_t N, int G, double *__restrict__ z_out,
                 int32_t *__restrict__ status_out, double *__restrict__ returns_out,
                 int32_t *__restrict__ bottleneck_out, double *__restrict__ arrival_out,
-                double *__restrict__ time_out, int32_t *__restrict__ q0_out) {
+                double *__restrict__ time_out, int32_t *__restrict__ q0_out, int fixup) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int n = I.n, m = I.m, k = I.k, two_n = 2 * n;
-    const CandLayout CL = cand_layout(n, MODE);
     using TT = TimeT<INTD>;
+    using RT = typename std::conditional<NARROW, uint32_t, TT>::type;
+    const CandLayout CL = cand_layout(n, MODE, (int)sizeof(RT));
     TT *s_p = reinterpret_cast<TT *>(smem);
     unsigned char *wbase = smem + block_p_bytes(n) + (size_t)warp * G * CL.total;
 
@@ -159,7 +167,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     const unsigned gmask = glane ? (((m == 32) ? 0xffffffffu : ((1u << m) - 1u)) << (g * m)) : 0u;
     const int leader = g * m;  // lane holding route 0 of this lane's candidate
     unsigned char *cbase = wbase + (size_t)(glane ? g : 0) * CL.total;
-    TT *s_ready = reinterpret_cast<TT *>(cbase + CL.ready);
+    RT *s_ready = reinterpret_cast<RT *>(cbase + CL.ready);
     uint32_t *s_posd = reinterpret_cast<uint32_t *>(cbase + CL.posd);
 
     for (int c = threadIdx.x; c <= n; c += blockDim.x)
@@ -169,7 +177,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     const int64_t step = (int64_t)gridDim.x * wpb * G;
     for (int64_t base = ((int64_t)blockIdx.x * wpb + warp) * G; base < N; base += step) {
         const int64_t cand = base + g;
-        const bool live = glane && cand < N;
+        const bool live = glane && cand < N && (!fixup || status_out[cand] == ST_RETRY);
         // ---- route offsets: lane v sums the lengths of routes 0..v-1
         int L = 0, off = 0, total = 0;
         bool mal = false;
@@ -188,8 +196,8 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
 
         // ---- shared tables: ready = -1 (dropoff not done); validation bitmap
         for (int gg = 0; gg < G; ++gg) {
-            TT *rd = reinterpret_cast<TT *>(wbase + (size_t)gg * CL.total + CL.ready);
-            for (int c = lane; c <= n; c += 32) rd[c] = (TT)-1;
+            RT *rd = reinterpret_cast<RT *>(wbase + (size_t)gg * CL.total + CL.ready);
+            for (int c = lane; c <= n; c += 32) rd[c] = NARROW ? (RT)NOT_READY32 : (RT)-1;
             if (MODE != MODE_EXACT) {
                 uint32_t *bt = reinterpret_cast<uint32_t *>(wbase + (size_t)gg * CL.total + CL.bits);
                 for (int w = lane; w < (two_n + 31) / 32; w += 32) bt[w] = 0u;
@@ -223,7 +231,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         rs.init(I, row + off, run ? L : 0, two_n);
         TT t = 0;
         int s = 0, lo = 0, hi = k, lastc = 0;
-        bool dead = false, bad_ops = false;
+        bool dead = false, bad_ops = false, ovf = false;
 
         if (MODE == MODE_TWO) {
             // pass 1: no-wait walk; ready = dropoff time + p (schedule.py:371-378)
@@ -263,13 +271,22 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 const int op = active ? rs.o[0] : 0;
                 const int c = op_customer(op);
                 const bool pick = op & 1;
-                const TT r = s_ready[c];
+                const RT rraw = s_ready[c];
+                const TT r = NARROW ? (rraw == (RT)NOT_READY32 ? (TT)-1 : (TT)rraw) : (TT)rraw;
                 const TT pc = s_p[c];
                 const bool go = active && !(pick && r < (TT)0);
                 const TT arr = t + rs.leg0();
                 const TT tn = (pick && !(arr >= r)) ? r : arr;
                 if (go) {
-                    if (!pick) s_ready[c] = tn + pc;
+                    if (!pick) {
+                        const TT rv = tn + pc;
+                        if (NARROW) {
+                            ovf |= (unsigned long long)rv >= (unsigned long long)NOT_READY32;
+                            s_ready[c] = (RT)rv;
+                        } else {
+                            s_ready[c] = (RT)rv;
+                        }
+                    }
                     if (REC) {
                         const int64_t at = cand * stride + off + rs.i;
                         arrival_out[at] = (double)arr;
@@ -293,7 +310,8 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         mal = mal || ((__ballot_sync(VRP_FULL_MASK, live && bad_ops) & gmask) != 0);
         const bool capfail = (__ballot_sync(VRP_FULL_MASK, live && lo > hi) & gmask) != 0;
         const bool gdead = (__ballot_sync(VRP_FULL_MASK, live && dead) & gmask) != 0;
-        const int st = mal ? ST_MAL : (capfail ? ST_CAP : (gdead ? ST_DEAD : ST_OK));
+        const bool govf = NARROW && (__ballot_sync(VRP_FULL_MASK, live && ovf) & gmask) != 0;
+        const int st = mal ? ST_MAL : (govf ? ST_RETRY : (capfail ? ST_CAP : (gdead ? ST_DEAD : ST_OK)));
 
         double ret = 0.0;
         if (live && st == ST_OK && L > 0) {
@@ -306,6 +324,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             z = x > z ? x : z;
         }
         const unsigned bm = __ballot_sync(VRP_FULL_MASK, live && ret == z) & gmask;
+        __syncwarp();  // every lane has read status_out (fixup) before lane 0 rewrites it
         if (live && v == 0) {
             z_out[cand] = st == ST_OK ? z : 0.0;
             status_out[cand] = st;
@@ -324,8 +343,8 @@ struct Shape {
 };
 
 template <typename Kern>
-int plan(Kern kern, int n, int m, int mode, Shape &out) {
-    const size_t per_cand = cand_layout(n, mode).total;
+int plan(Kern kern, int n, int m, int mode, int ready_bytes, Shape &out) {
+    const size_t per_cand = cand_layout(n, mode, ready_bytes).total;
     const size_t pbytes = block_p_bytes(n);
     const int gmax = 32 / m;
     long best = -1;
@@ -347,15 +366,17 @@ int plan(Kern kern, int n, int m, int mode, Shape &out) {
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)out.smem) == cudaSuccess ? 0 : -1;
 }
 
-template <typename OpT, bool INTD, int MODE, bool REC>
+template <typename OpT, bool INTD, int MODE, bool REC, bool NARROW>
 int launch_t(const DevInstance &I, const void *ops, int64_t stride, const int32_t *lens,
              int64_t N, double *z, int32_t *status, double *returns, int32_t *bottleneck,
-             double *arrival, double *timev, int32_t *q0, cudaStream_t stream, int sm_count) {
-    auto kern = makespan_kernel<OpT, INTD, MODE, REC>;
+             double *arrival, double *timev, int32_t *q0, cudaStream_t stream, int sm_count,
+             int fixup) {
+    auto kern = makespan_kernel<OpT, INTD, MODE, REC, NARROW>;
     static int cached_n = -1, cached_m = -1;
     static Shape sh;
     if (cached_n != I.n || cached_m != I.m) {
-        const int rc = plan(kern, I.n, I.m, MODE, sh);
+        using RT = typename std::conditional<NARROW, uint32_t, TimeT<INTD>>::type;
+        const int rc = plan(kern, I.n, I.m, MODE, (int)sizeof(RT), sh);
         if (rc) return rc;
         cached_n = I.n;
         cached_m = I.m;
@@ -367,8 +388,21 @@ int launch_t(const DevInstance &I, const void *ops, int64_t stride, const int32_
     if (grid < 1) grid = 1;
     kern<<<(unsigned)grid, 32 * sh.wpb, sh.smem, stream>>>(
         I, static_cast<const OpT *>(ops), stride, lens, N, sh.G, z, status, returns, bottleneck,
-        arrival, timev, q0);
+        arrival, timev, q0, fixup);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
+// integral exact/evaluate: narrow pass, then the 64-bit kernel over the
+// (normally zero) candidates whose ready times did not fit in 32 bits
+template <typename OpT, int MODE>
+int launch_narrow(const DevInstance &I, const void *ops, int64_t stride, const int32_t *lens,
+                  int64_t N, double *z, int32_t *status, double *returns, int32_t *bottleneck,
+                  cudaStream_t stream, int sm_count) {
+    int rc = launch_t<OpT, true, MODE, false, true>(I, ops, stride, lens, N, z, status, returns, bottleneck,
+                                                    nullptr, nullptr, nullptr, stream, sm_count, 0);
+    if (rc) return rc;
+    return launch_t<OpT, true, MODE, false, false>(I, ops, stride, lens, N, z, status, returns, bottleneck,
+                                                   nullptr, nullptr, nullptr, stream, sm_count, 1);
 }
 
 template <typename OpT, bool INTD>
@@ -377,18 +411,28 @@ int dispatch_mode(const DevInstance &I, const void *ops, int64_t stride, const i
                   int32_t *bottleneck, double *arrival, double *timev, int32_t *q0,
                   cudaStream_t stream, int sm_count) {
     if (rec)
-        return launch_t<OpT, INTD, MODE_EVAL, true>(I, ops, stride, lens, N, z, status, returns,
-                                                    bottleneck, arrival, timev, q0, stream, sm_count);
+        return launch_t<OpT, INTD, MODE_EVAL, true, false>(I, ops, stride, lens, N, z, status, returns,
+                                                           bottleneck, arrival, timev, q0, stream,
+                                                           sm_count, 0);
+    if (INTD && mode == MODE_EXACT)
+        return launch_narrow<OpT, MODE_EXACT>(I, ops, stride, lens, N, z, status, returns, bottleneck,
+                                              stream, sm_count);
+    if (INTD && mode == MODE_EVAL)
+        return launch_narrow<OpT, MODE_EVAL>(I, ops, stride, lens, N, z, status, returns, bottleneck,
+                                             stream, sm_count);
     switch (mode) {
         case MODE_EXACT:
-            return launch_t<OpT, INTD, MODE_EXACT, false>(I, ops, stride, lens, N, z, status, returns,
-                                                          bottleneck, nullptr, nullptr, nullptr, stream, sm_count);
+            return launch_t<OpT, INTD, MODE_EXACT, false, false>(I, ops, stride, lens, N, z, status, returns,
+                                                                 bottleneck, nullptr, nullptr, nullptr,
+                                                                 stream, sm_count, 0);
         case MODE_EVAL:
-            return launch_t<OpT, INTD, MODE_EVAL, false>(I, ops, stride, lens, N, z, status, returns,
-                                                         bottleneck, nullptr, nullptr, nullptr, stream, sm_count);
+            return launch_t<OpT, INTD, MODE_EVAL, false, false>(I, ops, stride, lens, N, z, status, returns,
+                                                                bottleneck, nullptr, nullptr, nullptr,
+                                                                stream, sm_count, 0);
         default:
-            return launch_t<OpT, INTD, MODE_TWO, false>(I, ops, stride, lens, N, z, status, returns,
-                                                        bottleneck, nullptr, nullptr, nullptr, stream, sm_count);
+            return launch_t<OpT, INTD, MODE_TWO, false, false>(I, ops, stride, lens, N, z, status, returns,
+                                                               bottleneck, nullptr, nullptr, nullptr,
+                                                               stream, sm_count, 0);
     }
 }
 

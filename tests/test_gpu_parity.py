@@ -129,3 +129,25 @@ def test_non_integral_instance_bit_exact():
         z, st = O.makespan_batch(inst, ops, lens, mode=name)
         np.testing.assert_array_equal(s["status"].cpu().numpy(), st)
         np.testing.assert_array_equal(s["z"].cpu().numpy(), z)
+
+
+def test_narrow_ready_overflow_falls_back_exactly():
+    """Integral instance whose ready times exceed 32 bits: the narrow K1 pass
+    must flag those candidates and the 64-bit fix-up pass reproduce the
+    oracle exactly (plus small-time candidates that stay on the narrow path)."""
+    from paper_2602_23685_b200.instance import Instance
+    base = config_instance("kroA100")
+    d, p = base.arrays()
+    p2 = np.minimum(p * 7000.0, 2.0**31 - 1)  # integral, < 2^31, sums overflow 2^32
+    inst = Instance.from_arrays(d, p2, base.m, base.k, label="kro-huge-p")
+    genes = I.chromosomes(inst.n, 512, (17, 17))
+    ref = O.decode_batch(inst, genes)
+    small = O.decode_batch(base, genes)
+    for mode, name in ((0, "exact"), (1, "evaluate")):
+        r = dev().makespan_batch(inst, _cuda(ref["ops"]), _cuda(ref["lens"]), mode=mode)
+        z, st = O.makespan_batch(inst, ref["ops"], ref["lens"], mode=name)
+        assert (z > 2.0**32).any()
+        np.testing.assert_array_equal(r["status"].cpu().numpy(), st)
+        np.testing.assert_array_equal(r["z"].cpu().numpy(), z)
+        r = dev().makespan_batch(base, _cuda(small["ops"]), _cuda(small["lens"]), mode=mode)
+        np.testing.assert_array_equal(r["z"].cpu().numpy(), small["makespan"])
