@@ -138,8 +138,8 @@ def test_narrow_ready_overflow_falls_back_exactly():
     from paper_2602_23685_b200.instance import Instance
     base = config_instance("kroA100")
     d, p = base.arrays()
-    p2 = np.minimum(p * 7000.0, 2.0**31 - 1)  # integral, < 2^31, sums overflow 2^32
-    inst = Instance.from_arrays(d, p2, base.m, base.k, label="kro-huge-p")
+    d2 = np.minimum(d * 100000.0, 2.0**31 - 1)  # integral, < 2^31; route sums pass 2^32
+    inst = Instance.from_arrays(d2, p, base.m, base.k, label="kro-huge-d")
     genes = I.chromosomes(inst.n, 512, (17, 17))
     ref = O.decode_batch(inst, genes)
     small = O.decode_batch(base, genes)
