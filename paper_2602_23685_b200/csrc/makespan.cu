@@ -39,6 +39,8 @@ constexpr int MODE_EXACT = 0, MODE_EVAL = 1, MODE_TWO = 2;
 constexpr int ST_OK = 0, ST_CAP = 1, ST_DEAD = 2, ST_MAL = 3;
 constexpr int ST_RETRY = 4;                 // internal: narrow ready table overflowed
 constexpr uint32_t NOT_READY32 = 0xFFFFFFFFu;
+constexpr int OPS_AHEAD = 8;   // op codes in registers (positions i .. i+7)
+constexpr int LEGS_AHEAD = 4;  // gathered legs in registers (positions i .. i+3)
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -93,18 +95,12 @@ using TimeT = typename std::conditional<INTD, long long, double>::type;
 
 template <typename OpT, bool INTD>
 struct RouteStream {
-    // Block-rotated register pipeline: positions are grouped in blocks of 4.
-    // oa/la hold the op codes / legs of the block containing position i, ob/lb
-    // the next block, oc the raw op codes of the block after.  The consumer
-    // selects oa[i&3], la[i&3]; registers only move at a block boundary, and
-    // every register moved there was loaded at the previous boundary (>= 4
-    // advances ago), so no move waits on an in-flight load.
     using LT = typename LegRaw<INTD>::T;
     using TT = TimeT<INTD>;
     const OpT *rp;
     int L, i, two_n;
-    int oa[4], ob[4], oc[4];
-    LT la[4], lb[4];
+    int o[OPS_AHEAD];
+    LT l[LEGS_AHEAD];
     bool bad;
 
     __device__ __forceinline__ int fetch(int pos) const { return pos < L ? (int)__ldg(rp + pos) : -1; }
@@ -118,39 +114,26 @@ struct RouteStream {
         if (op < 0) return (LT)0;
         return gather_leg<INTD>(I, prev_op < 0 ? 0 : op_customer(prev_op), op_customer(op));
     }
-    template <typename T>
-    __device__ __forceinline__ static T pick4(const T (&x)[4], int j) {
-        return j == 0 ? x[0] : (j == 1 ? x[1] : (j == 2 ? x[2] : x[3]));
-    }
-    __device__ __forceinline__ int cur_op() const { return pick4(oa, i & 3); }
-    __device__ __forceinline__ TT leg0() const { return (TT)pick4(la, i & 3); }
+    __device__ __forceinline__ TT leg0() const { return (TT)l[0]; }
     __device__ __forceinline__ void init(const DevInstance &I, const OpT *route, int len, int n2) {
         rp = route; L = len; i = 0; two_n = n2; bad = false;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) { oa[q] = fetch(q); ob[q] = fetch(4 + q); oc[q] = fetch(8 + q); }
+        for (int q = 0; q < OPS_AHEAD; ++q) o[q] = fetch(q);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) { oa[q] = checked(oa[q], q); ob[q] = checked(ob[q], 4 + q); }
-        la[0] = leg(I, -1, oa[0]);
+        for (int q = 0; q < LEGS_AHEAD; ++q) o[q] = checked(o[q], q);
+        l[0] = leg(I, -1, o[0]);
 #pragma unroll
-        for (int q = 1; q < 4; ++q) la[q] = leg(I, oa[q - 1], oa[q]);
-        lb[0] = leg(I, oa[3], ob[0]);
-#pragma unroll
-        for (int q = 1; q < 4; ++q) lb[q] = leg(I, ob[q - 1], ob[q]);
+        for (int q = 1; q < LEGS_AHEAD; ++q) l[q] = leg(I, o[q - 1], o[q]);
     }
     __device__ __forceinline__ void advance(const DevInstance &I) {
         ++i;
-        if ((i & 3) == 0) {
-            const int base = i + 4;  // first position of the new `ob` block
 #pragma unroll
-            for (int q = 0; q < 4; ++q) { oa[q] = ob[q]; la[q] = lb[q]; }
+        for (int q = 0; q + 1 < OPS_AHEAD; ++q) o[q] = o[q + 1];
+        o[OPS_AHEAD - 1] = fetch(i + OPS_AHEAD - 1);
+        o[LEGS_AHEAD - 1] = checked(o[LEGS_AHEAD - 1], i + LEGS_AHEAD - 1);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) ob[q] = checked(oc[q], base + q);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) oc[q] = fetch(base + 4 + q);
-            lb[0] = leg(I, oa[3], ob[0]);
-#pragma unroll
-            for (int q = 1; q < 4; ++q) lb[q] = leg(I, ob[q - 1], ob[q]);
-        }
+        for (int q = 0; q + 1 < LEGS_AHEAD; ++q) l[q] = l[q + 1];
+        l[LEGS_AHEAD - 1] = leg(I, o[LEGS_AHEAD - 2], o[LEGS_AHEAD - 1]);
     }
     // re-read and validate the op at `pos` (capacity scan past a deadlock)
     __device__ __forceinline__ int checked_at(int pos) { return checked(fetch(pos), pos); }
@@ -253,7 +236,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         if (MODE == MODE_TWO) {
             // pass 1: no-wait walk; ready = dropoff time + p (schedule.py:371-378)
             while (rs.i < rs.L) {
-                const int op = rs.cur_op();
+                const int op = rs.o[0];
                 const int c = op_customer(op);
                 t = t + rs.leg0();
                 if (!(op & 1)) {
@@ -271,7 +254,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             rs.init(I, row + off, run ? L : 0, two_n);
             t = 0;
             while (rs.i < rs.L) {
-                const int op = rs.cur_op();
+                const int op = rs.o[0];
                 const int c = op_customer(op);
                 t = t + rs.leg0();
                 if (op & 1) {
@@ -285,7 +268,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         } else {
             for (;;) {
                 const bool active = run && !dead && rs.i < rs.L;
-                const int op = active ? rs.cur_op() : 0;
+                const int op = active ? rs.o[0] : 0;
                 const int c = op_customer(op);
                 const bool pick = op & 1;
                 const RT rraw = s_ready[c];
