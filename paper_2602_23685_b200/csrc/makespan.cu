@@ -98,12 +98,14 @@ struct RouteStream {
     using LT = typename LegRaw<INTD>::T;
     using TT = TimeT<INTD>;
     const OpT *rp;
-    int L, i, two_n;
+    int L, i, two_n, lastp;
     int o[OPS_AHEAD];
     LT l[LEGS_AHEAD];
     bool bad;
 
-    __device__ __forceinline__ int fetch(int pos) const { return pos < L ? (int)__ldg(rp + pos) : -1; }
+    // Loads never feed a select: positions past the end re-read the last op
+    // (in bounds); the -1 sentinel is applied by checked() stages later.
+    __device__ __forceinline__ int fetch(int pos) const { return (int)__ldg(rp + (pos < L ? pos : lastp)); }
     // validate the op at route position `pos` (past the end -> -1 sentinel)
     __device__ __forceinline__ int checked(int op, int pos) {
         if (pos >= L) return -1;
@@ -117,6 +119,7 @@ struct RouteStream {
     __device__ __forceinline__ TT leg0() const { return (TT)l[0]; }
     __device__ __forceinline__ void init(const DevInstance &I, const OpT *route, int len, int n2) {
         rp = route; L = len; i = 0; two_n = n2; bad = false;
+        lastp = len > 0 ? len - 1 : 0;  // len == 0: rp points inside the row, never consumed
 #pragma unroll
         for (int q = 0; q < OPS_AHEAD; ++q) o[q] = fetch(q);
 #pragma unroll
@@ -228,7 +231,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         const bool run = live && !mal;
 
         RouteStream<OpT, INTD> rs;
-        rs.init(I, row + off, run ? L : 0, two_n);
+        rs.init(I, row + (run && L > 0 ? off : 0), run ? L : 0, two_n);
         TT t = 0;
         int s = 0, lo = 0, hi = k, lastc = 0;
         bool dead = false, bad_ops = false, ovf = false;
@@ -251,7 +254,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             __syncwarp();
             // pass 2: waits at pickups (schedule.py:380-393), and the same-route
             // pickup-before-its-dropoff Deadlock (:362-369)
-            rs.init(I, row + off, run ? L : 0, two_n);
+            rs.init(I, row + (run && L > 0 ? off : 0), run ? L : 0, two_n);
             t = 0;
             while (rs.i < rs.L) {
                 const int op = rs.o[0];
