@@ -33,26 +33,24 @@ __host__ __device__ inline int pow2_at_least(int x) {
     return p;
 }
 
+// Sort kernel smem per warp: P2 keys (u64) + P2 indices (u16).
+__host__ __device__ inline size_t sort_bytes(int n) {
+    const int P2 = pow2_at_least(2 * n);
+    return align16(8 * (size_t)P2) + align16(2 * (size_t)P2);
+}
+
+// Decode kernel smem per warp: the pending list and the ready table only --
+// the (op, vehicle) event log goes to a global scratch row, so residency is
+// set by 2*(2n) + 8*(n+1) bytes (12 KB at n = 999).
 struct DecodeLayout {
-    int P2;
-    size_t keys, ready, seq_op, seq_v, idx, total;
+    size_t pend, ready, total;
 };
 
-// region K: sort keys during the sort, then {ready, seq_op, seq_v};
-// region I: sort indices, then the pending list (in place).
 __host__ __device__ inline DecodeLayout decode_layout(int n) {
     DecodeLayout L;
-    const int two_n = 2 * n;
-    L.P2 = pow2_at_least(two_n);
-    L.keys = 0;
-    size_t after_sort = 0;
-    L.ready = after_sort; after_sort += align16(sizeof(double) * (size_t)(n + 1));
-    L.seq_op = after_sort; after_sort += align16(sizeof(uint16_t) * (size_t)two_n);
-    L.seq_v = after_sort; after_sort += align16((size_t)two_n);
-    size_t regionK = align16(sizeof(uint64_t) * (size_t)L.P2);
-    if (after_sort > regionK) regionK = after_sort;
-    L.idx = regionK;
-    L.total = regionK + align16(sizeof(uint16_t) * (size_t)L.P2);
+    L.pend = 0;
+    L.ready = align16(2 * (size_t)(2 * n));
+    L.total = L.ready + align16(8 * (size_t)(n + 1));
     return L;
 }
 
@@ -104,13 +102,39 @@ __device__ __forceinline__ void fleet_flags(bool vlane, double t, int net, int l
     pick_maxT = relax ? 0.0 : warp_max(cp ? t : -DBL_MAX);
 }
 
+// Stable argsort of every chromosome's 2n priorities (brkga.py:116), one warp
+// per chromosome; writes the order as u16 op indices to order_out[N][2n].
+__global__ void __launch_bounds__(256)
+sort_kernel(const double *__restrict__ genes, int64_t gstride, int64_t N, int two_n,
+            uint16_t *__restrict__ order_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    const int P2 = pow2_at_least(two_n);
+    unsigned char *base = smem + (size_t)warp * (align16(8 * (size_t)P2) + align16(2 * (size_t)P2));
+    uint64_t *s_key = reinterpret_cast<uint64_t *>(base);
+    uint16_t *s_idx = reinterpret_cast<uint16_t *>(base + align16(8 * (size_t)P2));
+    for (int64_t chrom = (int64_t)blockIdx.x * wpb + warp; chrom < N; chrom += (int64_t)gridDim.x * wpb) {
+        const double *g = genes + chrom * gstride;
+        for (int i = lane; i < P2; i += 32) {
+            s_key[i] = i < two_n ? order_key(__ldg(g + i)) : ~0ull;
+            s_idx[i] = (uint16_t)i;
+        }
+        __syncwarp();
+        bitonic_sort(s_key, s_idx, P2, lane);
+        uint16_t *o = order_out + chrom * (int64_t)two_n;
+        for (int i = lane; i < two_n; i += 32) o[i] = s_idx[i];
+        __syncwarp();
+    }
+}
+
 template <bool INTD, typename OutT>
 __global__ void __launch_bounds__(256, 1)
 decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, int64_t N,
               int relax, double penalty, double *__restrict__ fitness_out,
               double *__restrict__ makespan_out, int32_t *__restrict__ scheduled_out,
               int64_t *__restrict__ visits_out, OutT *__restrict__ ops_out, int64_t ostride,
-              int32_t *__restrict__ lens_out) {
+              int32_t *__restrict__ lens_out, const uint16_t *__restrict__ order,
+              uint32_t *__restrict__ seq_scratch) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -118,24 +142,18 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
     const int n = I.n, m = I.m, k = I.k, two_n = 2 * n;
     const DecodeLayout Ly = decode_layout(n);
     unsigned char *base = smem + (size_t)warp * Ly.total;
-    uint64_t *s_key = reinterpret_cast<uint64_t *>(base + Ly.keys);
     volatile double *s_ready = reinterpret_cast<volatile double *>(base + Ly.ready);
-    uint16_t *s_seq_op = reinterpret_cast<uint16_t *>(base + Ly.seq_op);
-    uint8_t *s_seq_v = reinterpret_cast<uint8_t *>(base + Ly.seq_v);
-    uint16_t *s_pend = reinterpret_cast<uint16_t *>(base + Ly.idx);
+    uint16_t *s_pend = reinterpret_cast<uint16_t *>(base + Ly.pend);
     const bool vlane = lane < m;
     const unsigned lt = lanemask_lt();
 
     for (int64_t chrom = (int64_t)blockIdx.x * wpb + warp; chrom < N;
          chrom += (int64_t)gridDim.x * wpb) {
         const double *g = genes + chrom * gstride;
-        // ---- stable argsort of the priorities
-        for (int i = lane; i < Ly.P2; i += 32) {
-            s_key[i] = i < two_n ? order_key(__ldg(g + i)) : ~0ull;
-            s_pend[i] = (uint16_t)i;
-        }
-        __syncwarp();
-        bitonic_sort(s_key, s_pend, Ly.P2, lane);
+        uint32_t *seq = seq_scratch + chrom * (int64_t)two_n;  // (op | vehicle << 16) log
+        // ---- pending list = the stable priority order (sort_kernel)
+        const uint16_t *ord = order + chrom * (int64_t)two_n;
+        for (int i = lane; i < two_n; i += 32) s_pend[i] = __ldg(ord + i);
         for (int c = lane; c <= n; c += 32) s_ready[c] = -1.0;  // -1: not dropped
         __syncwarp();
 
@@ -221,8 +239,7 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
                     }
                     if (lane == 0) {
                         if (!pickf) s_ready[cf] = cstar + __ldg(I.p + cf);
-                        s_seq_op[nseq] = (uint16_t)opf;
-                        s_seq_v[nseq] = (uint8_t)vstar;
+                        if (seq_scratch) seq[nseq] = (uint32_t)opf | ((uint32_t)vstar << 16);
                     }
                     ++nseq;
                     progressed = true;
@@ -257,8 +274,9 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
             for (int sb = 0; sb < nseq; sb += 32) {
                 const int j = sb + lane;
                 const bool valid = j < nseq;
-                const int op = valid ? s_seq_op[j] : 0;
-                const int v = valid ? s_seq_v[j] : -1;
+                const uint32_t e = valid ? seq[j] : 0u;
+                const int op = (int)(e & 0xffffu);
+                const int v = valid ? (int)(e >> 16) : -1;
                 for (int u = 0; u < m; ++u) {
                     const unsigned mk = __ballot_sync(VRP_FULL_MASK, v == u);
                     const int ou = __shfl_sync(VRP_FULL_MASK, off, u);
@@ -297,6 +315,29 @@ int launch_t(const DevInstance &I, const double *genes, int64_t gstride, int64_t
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per_warp * best_w));
         cached_pw = per_warp; cached_w = best_w; cached_blocks = best_blocks;
     }
+    // scratch: priority order (u16) and, when the solution is wanted, the
+    // (op | vehicle << 16) event log
+    const int two_n = 2 * I.n;
+    uint16_t *order = nullptr;
+    uint32_t *seq = nullptr;
+    if (cudaMallocAsync(&order, sizeof(uint16_t) * (size_t)N * two_n, stream) != cudaSuccess) return -1;
+    if (ops_out && cudaMallocAsync(&seq, sizeof(uint32_t) * (size_t)N * two_n, stream) != cudaSuccess) return -1;
+    {
+        static int sort_n = -1;
+        const int sw = 4;
+        const size_t sbytes = sort_bytes(I.n) * sw;
+        if (sort_n != I.n) {
+            if (cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbytes) != cudaSuccess)
+                return -1;
+            sort_n = I.n;
+        }
+        int sblocks = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sblocks, sort_kernel, 32 * sw, sbytes);
+        int64_t sgrid = (int64_t)(sblocks > 0 ? sblocks : 1) * sm_count;
+        const int64_t swant = (N + sw - 1) / sw;
+        if (sgrid > swant) sgrid = swant;
+        sort_kernel<<<(unsigned)sgrid, 32 * sw, sbytes, stream>>>(genes, gstride, N, two_n, order);
+    }
     const size_t bytes = per_warp * (size_t)cached_w;
     int64_t want = (N + cached_w - 1) / cached_w;
     int64_t grid = (int64_t)cached_blocks * sm_count;
@@ -304,8 +345,12 @@ int launch_t(const DevInstance &I, const double *genes, int64_t gstride, int64_t
     if (grid < 1) grid = 1;
     kern<<<(unsigned)grid, 32 * cached_w, bytes, stream>>>(I, genes, gstride, N, relax, penalty, fitness,
                                                          makespan, scheduled, visits,
-                                                         static_cast<OutT *>(ops_out), ostride, lens_out);
-    return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+                                                         static_cast<OutT *>(ops_out), ostride, lens_out,
+                                                         order, seq);
+    const cudaError_t e = cudaPeekAtLastError();
+    cudaFreeAsync(order, stream);
+    if (seq) cudaFreeAsync(seq, stream);
+    return e == cudaSuccess ? 0 : -1;
 }
 
 }  // namespace
