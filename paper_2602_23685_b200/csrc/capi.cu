@@ -70,6 +70,15 @@ int vrp_instance_create(int32_t n, int32_t m, int32_t k, const double *d_host, c
     if (!h) return fail(VRP_EINVAL, "out of host memory%s");
     cudaError_t e = cudaGetDevice(&h->device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device);
+    if (e == cudaSuccess) {
+        // kernels take their scratch from the stream-ordered pool; keep freed
+        // blocks cached instead of unmapping them at every synchronisation
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, h->device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
     if (e == cudaSuccess) e = cudaMalloc(&h->d, cells * sizeof(double));
     if (e == cudaSuccess) e = cudaMalloc(&h->p, (size_t)(n + 1) * sizeof(double));
     if (e == cudaSuccess) e = cudaMemcpy(h->d, d_host, cells * sizeof(double), cudaMemcpyHostToDevice);
