@@ -39,6 +39,8 @@ constexpr int MODE_EXACT = 0, MODE_EVAL = 1, MODE_TWO = 2;
 constexpr int ST_OK = 0, ST_CAP = 1, ST_DEAD = 2, ST_MAL = 3;
 constexpr int ST_RETRY = 4;                 // internal: narrow ready table overflowed
 constexpr uint32_t NOT_READY32 = 0xFFFFFFFFu;
+constexpr int OPS_AHEAD = 8;   // op codes in registers (positions i .. i+7)
+constexpr int LEGS_AHEAD = 4;  // gathered legs in registers (positions i .. i+3)
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -91,36 +93,14 @@ __device__ __forceinline__ typename LegRaw<INTD>::T gather_leg(const DevInstance
 template <bool INTD>
 using TimeT = typename std::conditional<INTD, long long, double>::type;
 
-__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
-                 "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
-                 "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
-constexpr int OPS_AHEAD = 8;    // op codes in registers (positions i .. i+7)
-constexpr int LEGS_AHEAD = 4;   // legs in flight (positions i .. i+3)
-constexpr int LEG_RING = 8;     // per-lane shared-memory ring slots (power of two)
-
 template <typename OpT, bool INTD>
 struct RouteStream {
-    // Op codes stream through registers (read-only path; an L1 hit by the time
-    // they are shifted).  Legs d[prev][c] are gathered from L2 with cp.async
-    // straight into a per-lane shared-memory ring, LEGS_AHEAD positions ahead:
-    // no register ever holds an in-flight gather, so no shift or consumer waits
-    // on one -- the walk only waits (cp.async.wait_group) for the leg it is
-    // about to use, issued LEGS_AHEAD advances earlier.
     using LT = typename LegRaw<INTD>::T;
     using TT = TimeT<INTD>;
     const OpT *rp;
-    LT *ring;
     int L, i, two_n, lastp;
     int o[OPS_AHEAD];
+    LT l[LEGS_AHEAD];
     bool bad;
 
     // Loads never feed a select: positions past the end re-read the last op
@@ -132,36 +112,31 @@ struct RouteStream {
         if ((unsigned)op >= (unsigned)two_n) { bad = true; return 0; }
         return op;
     }
-    // gather the leg of position pos (op `op`, predecessor `prev_op`) into its slot
-    __device__ __forceinline__ void gather(const DevInstance &I, int pos, int prev_op, int op) {
-        if (op >= 0) {
-            const int64_t idx = (int64_t)(prev_op < 0 ? 0 : op_customer(prev_op)) * I.W + op_customer(op);
-            if (INTD) cp_async4(ring + (pos & (LEG_RING - 1)), I.d32 + idx);
-            else cp_async8(ring + (pos & (LEG_RING - 1)), I.d + idx);
-        }
-        cp_commit();
+    __device__ __forceinline__ LT leg(const DevInstance &I, int prev_op, int op) const {
+        if (op < 0) return (LT)0;
+        return gather_leg<INTD>(I, prev_op < 0 ? 0 : op_customer(prev_op), op_customer(op));
     }
-    __device__ __forceinline__ TT leg0() const { return (TT)ring[i & (LEG_RING - 1)]; }
-    __device__ __forceinline__ void init(const DevInstance &I, const OpT *route, int len, int n2, LT *lane_ring) {
-        rp = route; L = len; i = 0; two_n = n2; bad = false; ring = lane_ring;
+    __device__ __forceinline__ TT leg0() const { return (TT)l[0]; }
+    __device__ __forceinline__ void init(const DevInstance &I, const OpT *route, int len, int n2) {
+        rp = route; L = len; i = 0; two_n = n2; bad = false;
         lastp = len > 0 ? len - 1 : 0;  // len == 0: rp points inside the row, never consumed
 #pragma unroll
         for (int q = 0; q < OPS_AHEAD; ++q) o[q] = fetch(q);
 #pragma unroll
         for (int q = 0; q < LEGS_AHEAD; ++q) o[q] = checked(o[q], q);
-        gather(I, 0, -1, o[0]);
+        l[0] = leg(I, -1, o[0]);
 #pragma unroll
-        for (int q = 1; q < LEGS_AHEAD; ++q) gather(I, q, o[q - 1], o[q]);
+        for (int q = 1; q < LEGS_AHEAD; ++q) l[q] = leg(I, o[q - 1], o[q]);
     }
-    // make the leg of position i visible (at most LEGS_AHEAD-1 younger groups pending)
-    __device__ __forceinline__ void wait_leg() const { cp_wait<LEGS_AHEAD - 1>(); }
     __device__ __forceinline__ void advance(const DevInstance &I) {
         ++i;
 #pragma unroll
         for (int q = 0; q + 1 < OPS_AHEAD; ++q) o[q] = o[q + 1];
         o[OPS_AHEAD - 1] = fetch(i + OPS_AHEAD - 1);
         o[LEGS_AHEAD - 1] = checked(o[LEGS_AHEAD - 1], i + LEGS_AHEAD - 1);
-        gather(I, i + LEGS_AHEAD - 1, o[LEGS_AHEAD - 2], o[LEGS_AHEAD - 1]);
+#pragma unroll
+        for (int q = 0; q + 1 < LEGS_AHEAD; ++q) l[q] = l[q + 1];
+        l[LEGS_AHEAD - 1] = leg(I, o[LEGS_AHEAD - 2], o[LEGS_AHEAD - 1]);
     }
     // re-read and validate the op at `pos` (capacity scan past a deadlock)
     __device__ __forceinline__ int checked_at(int pos) { return checked(fetch(pos), pos); }
@@ -188,10 +163,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     using RT = typename std::conditional<NARROW, uint32_t, TT>::type;
     const CandLayout CL = cand_layout(n, MODE, (int)sizeof(RT));
     TT *s_p = reinterpret_cast<TT *>(smem);
-    using LTk = typename LegRaw<INTD>::T;
-    const size_t ring_bytes = align16(32 * LEG_RING * sizeof(LTk));
-    unsigned char *wbase = smem + block_p_bytes(n) + (size_t)warp * (G * CL.total + ring_bytes);
-    LTk *lane_ring = reinterpret_cast<LTk *>(wbase + (size_t)G * CL.total) + lane * LEG_RING;
+    unsigned char *wbase = smem + block_p_bytes(n) + (size_t)warp * G * CL.total;
 
     const int g = lane / m, v = lane - (lane / m) * m;
     const bool glane = g < G;
@@ -259,8 +231,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         const bool run = live && !mal;
 
         RouteStream<OpT, INTD> rs;
-        cp_wait<0>();
-        rs.init(I, row + (run && L > 0 ? off : 0), run ? L : 0, two_n, lane_ring);
+        rs.init(I, row + (run && L > 0 ? off : 0), run ? L : 0, two_n);
         TT t = 0;
         int s = 0, lo = 0, hi = k, lastc = 0;
         bool dead = false, bad_ops = false, ovf = false;
@@ -270,7 +241,6 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             while (rs.i < rs.L) {
                 const int op = rs.o[0];
                 const int c = op_customer(op);
-                rs.wait_leg();
                 t = t + rs.leg0();
                 if (!(op & 1)) {
                     s_ready[c] = t + s_p[c];
@@ -284,13 +254,11 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             __syncwarp();
             // pass 2: waits at pickups (schedule.py:380-393), and the same-route
             // pickup-before-its-dropoff Deadlock (:362-369)
-            cp_wait<0>();
-        rs.init(I, row + (run && L > 0 ? off : 0), run ? L : 0, two_n, lane_ring);
+            rs.init(I, row + (run && L > 0 ? off : 0), run ? L : 0, two_n);
             t = 0;
             while (rs.i < rs.L) {
                 const int op = rs.o[0];
                 const int c = op_customer(op);
-                rs.wait_leg();
                 t = t + rs.leg0();
                 if (op & 1) {
                     const TT r = s_ready[c];
@@ -310,7 +278,6 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 const TT r = NARROW ? (rraw == (RT)NOT_READY32 ? (TT)-1 : (TT)rraw) : (TT)rraw;
                 const TT pc = s_p[c];
                 const bool go = active && !(pick && r < (TT)0);
-                rs.wait_leg();
                 const TT arr = t + rs.leg0();
                 const TT tn = (pick && !(arr >= r)) ? r : arr;
                 if (go) {
@@ -368,7 +335,6 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         }
         if (live && returns_out) returns_out[cand * m + v] = st == ST_OK ? ret : 0.0;
         if (REC && live && q0_out) q0_out[cand * m + v] = lo;
-        cp_wait<0>();
         __syncwarp();
     }
 }
@@ -380,15 +346,14 @@ struct Shape {
 };
 
 template <typename Kern>
-int plan(Kern kern, int n, int m, int mode, int ready_bytes, int leg_bytes, Shape &out) {
+int plan(Kern kern, int n, int m, int mode, int ready_bytes, Shape &out) {
     const size_t per_cand = cand_layout(n, mode, ready_bytes).total;
-    const size_t ring = align16(32 * LEG_RING * (size_t)leg_bytes);
     const size_t pbytes = block_p_bytes(n);
     const int gmax = 32 / m;
     long best = -1;
     for (int G = gmax; G >= 1; --G) {
         for (int w = 8; w >= 1; --w) {
-            const size_t bytes = pbytes + (size_t)w * (G * per_cand + ring);
+            const size_t bytes = pbytes + (size_t)w * G * per_cand;
             if (bytes > 227 * 1024) continue;
             if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
                 return -1;
@@ -414,7 +379,7 @@ int launch_t(const DevInstance &I, const void *ops, int64_t stride, const int32_
     static Shape sh;
     if (cached_n != I.n || cached_m != I.m) {
         using RT = typename std::conditional<NARROW, uint32_t, TimeT<INTD>>::type;
-        const int rc = plan(kern, I.n, I.m, MODE, (int)sizeof(RT), INTD ? 4 : 8, sh);
+        const int rc = plan(kern, I.n, I.m, MODE, (int)sizeof(RT), sh);
         if (rc) return rc;
         cached_n = I.n;
         cached_m = I.m;
