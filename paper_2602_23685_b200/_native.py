@@ -6,10 +6,12 @@ visible, every device entry point raises :class:`NativeUnavailable`.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "lib" / "libvrprpd.so"
+# VRP_LIB overrides the library path (side builds for ablation experiments)
+LIB_PATH = Path(os.environ["VRP_LIB"]) if os.environ.get("VRP_LIB") else PKG / "lib" / "libvrprpd.so"
 
 VRP_OK, VRP_CAPACITY, VRP_DEADLOCK, VRP_MALFORMED = 0, 1, 2, 3
 VRP_EINVAL, VRP_ECUDA, VRP_EUNSUPPORTED = 1, 2, 3
