@@ -146,6 +146,60 @@ int vrp_repair_batch(vrp_instance_t h, const int32_t *partial_ops, int64_t parti
                      int32_t *out_ops, int64_t out_stride, int32_t *out_lens, int32_t *status,
                      int64_t N, void *stream);
 
+/* K6: alns.destroy (alns.py:182-251) followed by insertion.remove_customers
+ * (insertion.py:379-397, capacity cascade included) on N solutions.
+ *   ops[N][op_stride] + lens[N][m]  complete solutions (vehicle-major, DEVICE)
+ *   opcode[N]: 0 random, 1 worst, 2 shaw, 3 cluster, 4 route, 5 critical_path
+ *   q[N] (clamped to n), q_min = removal_bounds(n)[0]
+ *   states[N]: per-solution generators (DEVICE), advanced like the reference's rng
+ *   out_ops[N][out_stride] (-1 padded) + out_lens[N][m]: the partial solutions
+ *   removed[N][removed_stride] (>= n) sorted removed customers, nremoved[N] */
+int vrp_destroy_batch(vrp_instance_t h, const int32_t *ops, int64_t op_stride, const int32_t *lens,
+                      const int32_t *opcode, const int32_t *q, int32_t q_min, vrp_philox *states,
+                      int32_t *out_ops, int64_t out_stride, int32_t *out_lens, int32_t *removed,
+                      int64_t removed_stride, int32_t *nremoved, int64_t N, void *stream);
+
+/* One ALNS worker (alns.py:536-640 run_alns locals), DEVICE-resident.
+ * weights/scores/attempts are indexed in the reference's operator order:
+ * random, worst, shaw, cluster, route, critical_path, greedy, regret2,
+ * regret3, regretm (alns.py:28-29). */
+typedef struct {
+    vrp_philox rng;           /* the worker's generator (alns.py:541) */
+    double z, z_best, temperature, t_init;
+    double weights[10], scores[10];
+    int64_t attempts[10];
+    int64_t stagnation, accepted, rejected, reheats;
+    int64_t best_it;          /* iteration of the last z_best improvement */
+    int32_t n_trace, n_rows;  /* records written by the last vrp_alns_iterate */
+} vrp_alns_worker;
+
+/* AlnsParams (alns.py:42-70) fields the device loop reads. */
+typedef struct {
+    double t0, alpha, reheat_factor, reaction, sigma1, sigma2, sigma3, min_weight;
+    int64_t stagnation_threshold, weight_interval;
+    int32_t q_min; /* min(removal_bounds(n)[0], n) (alns.py:102-109, :190) */
+    int32_t reserved;
+} vrp_alns_params;
+
+/* K6 + device-resident ALNS: iterations it_begin..it_end (1-based, inclusive)
+ * of run_alns's loop body (alns.py:566-611: roulette, destroy, repair,
+ * exact_makespan, SA acceptance, cooling/reheat, update_weights) for nw
+ * independent workers, one warp each.  Host-side steps (local search every
+ * pickup_reposition / cross_agent interval, pool share polling) belong at the
+ * iteration boundaries the caller chooses.
+ *   workers[nw]                      device, in/out
+ *   cur_ops/best_ops[nw][2n], cur_lens/best_lens[nw][m]  device, in/out (vehicle-major)
+ *   q_draws[nw][q_stride]            device: the worker's pre-drawn q (alns.py:556)
+ *   trace_it/trace_z[nw][trace_cap]  out: (iteration, z_best) per improvement
+ *   rows_it[nw][rows_cap], rows_val[nw][rows_cap][12]  out: weight rows
+ *                                    (z_best, temperature, 10 weights)
+ * workers[i].n_trace / n_rows receive the record counts of this call. */
+int vrp_alns_iterate(vrp_instance_t h, const vrp_alns_params *params, vrp_alns_worker *workers,
+                     int32_t nw, int32_t *cur_ops, int32_t *cur_lens, int32_t *best_ops,
+                     int32_t *best_lens, const int32_t *q_draws, int64_t q_stride, int64_t it_begin,
+                     int64_t it_end, int32_t *trace_it, double *trace_z, int64_t trace_cap,
+                     int32_t *rows_it, double *rows_val, int64_t rows_cap, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

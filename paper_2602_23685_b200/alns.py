@@ -493,12 +493,14 @@ class _PoolShare:
 
 class _Worker:
     """One ALNS trajectory (alns.py:536-640) split into phases so that many
-    workers can share the device launches of an iteration."""
+    workers can share the device launches of an iteration (host engine), or
+    so that the device engine can hand the host its boundary steps."""
 
     def __init__(self, instance, params: AlnsParams, seed: int, initial=None, share=None,
                  global_share=None, worker_id: int = 0, rng=None):
         self.instance, self.params = instance, params
         self.rng = rng if rng is not None else _rng_for(seed)
+        self._cur_arr = self._best_arr = None
         self.current = initial if initial is not None else construct_initial(instance, seed)
         self.z = exact_makespan(instance, self.current)
         self.best, self.z_best = self.current, self.z
@@ -506,6 +508,7 @@ class _Worker:
         self.t_init = self.temperature
         self.bank = OperatorBank.fresh()
         self.stagnation = 0
+        self.best_it = 0
         q_min, q_max = removal_bounds(instance.n)
         q_min, q_max = min(q_min, instance.n), min(q_max, instance.n)
         self.stats = AlnsStats(initial_makespan=self.z)
@@ -514,14 +517,36 @@ class _Worker:
                         if params.max_iter else [])
         self.share, self.global_share, self.worker_id = share, global_share, worker_id
 
+    # current / best are materialised lazily from device arrays (device engine)
+    @property
+    def current(self):
+        if self._current is None:
+            self._current = Solution.from_arrays(*self._cur_arr)
+        return self._current
+
+    @current.setter
+    def current(self, sol):
+        self._current, self._cur_arr, self.cur_dirty = sol, None, True
+
+    @property
+    def best(self):
+        if self._best is None:
+            self._best = Solution.from_arrays(*self._best_arr)
+        return self._best
+
+    @best.setter
+    def best(self, sol):
+        self._best, self._best_arr, self.best_dirty = sol, None, True
+
     def _found_best(self, sol, value, it):
         self.best, self.z_best = sol, value
+        self.best_it = it
         self.stagnation = 0
         self.stats.best_trace.append((it, value))
         if self.share is not None:
             self.share.offer(self.worker_id, value, sol)
 
-    # phase 1: operator selection + destroy (host)
+    # phase 1: operator selection + destroy (host engine)
     def propose(self, it: int):
         bank, rng = self.bank, self.rng
         self.dname = roulette_select(DESTROY_OPERATORS, bank.weights, rng)
@@ -538,8 +563,13 @@ class _Worker:
             raise ValueError(f"unknown repair operator {self.rname!r}")
         return not self.failed
 
-    # phase 3: acceptance + bookkeeping (host), given the repaired candidate
+    # phase 3: acceptance + bookkeeping, given the repaired candidate
     def conclude(self, it: int, cand, z_cand, failed: bool):
+        self.accept(it, cand, z_cand, failed)
+        self.post(it)
+
+    def accept(self, it: int, cand, z_cand, failed: bool):
+        """alns.py:577-611 -- what the device engine runs inside the kernel."""
         p, bank = self.params, self.bank
         if failed:
             self.stats.rejected_candidates += 1
@@ -565,10 +595,16 @@ class _Worker:
             self.stats.reheats += 1
         if it % p.weight_interval == 0:
             update_weights(bank, p.reaction, p.min_weight)
-            self.stats.weight_rows.append({"iteration": it, "best_makespan": self.z_best,
-                                           "temperature": self.temperature,
-                                           **{f"w_{k}": bank.weights[k] for k in bank.weights}})
-        inst = self.instance
+            self._weight_row(it, self.z_best, self.temperature, [bank.weights[k] for k in bank.weights])
+
+    def _weight_row(self, it, z_best, temperature, weights):
+        self.stats.weight_rows.append({"iteration": it, "best_makespan": z_best,
+                                       "temperature": temperature,
+                                       **{f"w_{k}": w for k, w in zip(self.bank.weights, weights)}})
+
+    def post(self, it: int):
+        """alns.py:612-640: local search, pool share polling and merging."""
+        p, inst = self.params, self.instance
         if it % p.pickup_reposition_interval == 0:
             improved = pickup_repositioning(inst, self.current)
             z_new = exact_makespan(inst, improved)
@@ -593,11 +629,171 @@ class _Worker:
         if self.share is not None and self.global_share is not None and it % p.pool_sync_interval == 0:
             self.share.merge(self.global_share)
 
+    def host_step(self, it: int) -> bool:
+        """Does post(it) have anything to do?"""
+        p = self.params
+        return (it % p.pickup_reposition_interval == 0 or it % p.cross_agent_interval == 0
+                or (self.share is not None and (it % p.best_check_interval == 0 or (
+                    self.global_share is not None and it % p.pool_sync_interval == 0))))
+
+    # device engine: worker <-> vrp_alns_worker record
+    def to_record(self, rec):
+        rec["rng"] = R.state_bytes(self.rng)
+        rec["z"], rec["z_best"] = self.z, self.z_best
+        rec["temperature"], rec["t_init"] = self.temperature, self.t_init
+        names = list(self.bank.weights)
+        rec["weights"] = [self.bank.weights[k] for k in names]
+        rec["scores"] = [self.bank.scores[k] for k in names]
+        rec["attempts"] = [self.bank.attempts[k] for k in names]
+        rec["stagnation"] = self.stagnation
+        rec["accepted"] = self.stats.accepted
+        rec["rejected"] = self.stats.rejected_candidates
+        rec["reheats"] = self.stats.reheats
+        rec["best_it"] = self.best_it
+        rec["n_trace"] = rec["n_rows"] = 0
+
+    def from_record(self, rec, trace, rows, cur_arr, best_arr):
+        R.set_state_bytes(self.rng, rec["rng"])
+        self.z, self.z_best = float(rec["z"]), float(rec["z_best"])
+        self.temperature, self.t_init = float(rec["temperature"]), float(rec["t_init"])
+        names = list(self.bank.weights)
+        for j, k in enumerate(names):
+            self.bank.weights[k] = float(rec["weights"][j])
+            self.bank.scores[k] = float(rec["scores"][j])
+            self.bank.attempts[k] = int(rec["attempts"][j])
+        self.stagnation = int(rec["stagnation"])
+        self.stats.accepted = int(rec["accepted"])
+        self.stats.rejected_candidates = int(rec["rejected"])
+        self.stats.reheats = int(rec["reheats"])
+        self.best_it = int(rec["best_it"])
+        self.stats.best_trace.extend(trace)
+        for it, vals in rows:
+            self._weight_row(it, vals[0], vals[1], vals[2:])
+        self._current, self._cur_arr, self.cur_dirty = None, cur_arr, False
+        if trace:
+            self._best, self._best_arr, self.best_dirty = None, best_arr, False
+
     def finish(self):
         self.stats.iterations = self.params.max_iter
         self.stats.attempts = dict(self.bank.attempts)
         self.stats.final_temperature = self.temperature
         return self.best, self.stats
+
+
+class _DeviceWorkers:
+    """Device-resident state of a list of workers driven by vrp_alns_iterate
+    (csrc/alns_step.cu).  The kernel runs stretches of iterations; the host
+    steps in only at iterations where post() has work (local search, share
+    polling/merging), in worker order, exactly where the sequential loop
+    would."""
+
+    def __init__(self, instance, params: AlnsParams, workers):
+        import torch
+        from . import device as DV
+        self.DV, self.torch = DV, torch
+        self.instance, self.params, self.workers = instance, params, workers
+        n, m, W = instance.n, instance.m, len(workers)
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.cparams = DV.AlnsParamsC(
+            t0=params.t0, alpha=params.alpha, reheat_factor=params.reheat_factor,
+            reaction=params.reaction, sigma1=params.sigma1, sigma2=params.sigma2,
+            sigma3=params.sigma3, min_weight=params.min_weight,
+            stagnation_threshold=params.stagnation_threshold, weight_interval=params.weight_interval,
+            q_min=min(removal_bounds(n)[0], n), reserved=0)
+        self.rec = np.zeros(W, DV.ALNS_WORKER_DTYPE)
+        cur = [w.current.to_arrays(n) for w in workers]
+        best = [w.best.to_arrays(n) for w in workers]
+        self.g_cur_ops = torch.from_numpy(np.stack([o[:2 * n] for o, _ in cur])).to(self.dev)
+        self.g_cur_lens = torch.from_numpy(np.stack([l for _, l in cur])).to(self.dev)
+        self.g_best_ops = torch.from_numpy(np.stack([o[:2 * n] for o, _ in best])).to(self.dev)
+        self.g_best_lens = torch.from_numpy(np.stack([l for _, l in best])).to(self.dev)
+        self.g_q = torch.from_numpy(np.stack([np.asarray(w.q_draws, np.int32) for w in workers])).to(self.dev)
+        self.g_rec = torch.empty((W, DV.ALNS_WORKER_DTYPE.itemsize), dtype=torch.uint8, device=self.dev)
+        self._cap = 0
+        for w in workers:
+            w.cur_dirty = w.best_dirty = False
+        self.push()
+
+    def _buffers(self, length):
+        if length > self._cap:
+            torch, W = self.torch, len(self.workers)
+            self._cap = length
+            rcap = length // self.params.weight_interval + 2
+            self.t_it = torch.empty((W, length), dtype=torch.int32, device=self.dev)
+            self.t_z = torch.empty((W, length), dtype=torch.float64, device=self.dev)
+            self.r_it = torch.empty((W, rcap), dtype=torch.int32, device=self.dev)
+            self.r_val = torch.empty((W, rcap, 12), dtype=torch.float64, device=self.dev)
+
+    def push(self):
+        n = self.instance.n
+        for i, w in enumerate(self.workers):
+            w.to_record(self.rec[i])
+            if w.cur_dirty:
+                o, l = w.current.to_arrays(n)
+                self.g_cur_ops[i].copy_(self.torch.from_numpy(o[:2 * n]))
+                self.g_cur_lens[i].copy_(self.torch.from_numpy(l))
+                w.cur_dirty = False
+            if w.best_dirty:
+                o, l = w.best.to_arrays(n)
+                self.g_best_ops[i].copy_(self.torch.from_numpy(o[:2 * n]))
+                self.g_best_lens[i].copy_(self.torch.from_numpy(l))
+                w.best_dirty = False
+        self.g_rec.copy_(self.torch.from_numpy(self.rec.view(np.uint8).reshape(len(self.workers), -1)))
+
+    def run(self, a: int, b: int):
+        """Iterations a..b on the device, then pull the state back."""
+        self._buffers(b - a + 1)
+        self.DV.alns_iterate(self.instance, self.cparams, self.g_rec, self.g_cur_ops, self.g_cur_lens,
+                             self.g_best_ops, self.g_best_lens, self.g_q, a, b, self.t_it, self.t_z,
+                             self.r_it, self.r_val)
+        rec = self.g_rec.cpu().numpy().view(self.DV.ALNS_WORKER_DTYPE).reshape(-1)
+        t_it, t_z = self.t_it.cpu().numpy(), self.t_z.cpu().numpy()
+        r_it, r_val = self.r_it.cpu().numpy(), self.r_val.cpu().numpy()
+        cur_o, cur_l = self.g_cur_ops.cpu().numpy(), self.g_cur_lens.cpu().numpy()
+        best_o, best_l = self.g_best_ops.cpu().numpy(), self.g_best_lens.cpu().numpy()
+        improved = []
+        for i, w in enumerate(self.workers):
+            nt, nr = int(rec[i]["n_trace"]), int(rec[i]["n_rows"])
+            trace = [(int(t_it[i, j]), float(t_z[i, j])) for j in range(nt)]
+            rows = [(int(r_it[i, j]), [float(x) for x in r_val[i, j]]) for j in range(nr)]
+            w.from_record(rec[i], trace, rows, (cur_o[i], cur_l[i]), (best_o[i], best_l[i]))
+            if nt:
+                improved.append(i)
+        self.rec = rec.copy()
+        return improved
+
+    def drive(self, stop=None, max_stretch: int | None = None):
+        """Run to max_iter (or until ``stop()`` is true at a stretch end)."""
+        p, workers = self.params, self.workers
+        pooled = workers[0].share is not None
+        it = 1
+        while it <= p.max_iter:
+            b = it
+            while (b < p.max_iter and not workers[0].host_step(b)
+                   and (max_stretch is None or b - it + 1 < max_stretch)):
+                b += 1
+            if pooled:
+                # offers made before b reach the shares before anyone polls at b,
+                # in (iteration, worker) order; b's own offers interleave with post(b)
+                if b > it:
+                    pre = self.run(it, b - 1)
+                    for i in sorted(pre, key=lambda i: (workers[i].best_it, i)):
+                        w = workers[i]
+                        w.share.offer(w.worker_id, w.z_best, w.best)
+                at_b = set(self.run(b, b))
+                for i, w in enumerate(workers):
+                    if i in at_b:
+                        w.share.offer(w.worker_id, w.z_best, w.best)
+                    w.post(b)
+            else:
+                self.run(it, b)
+                for w in workers:
+                    w.post(b)
+            self.push()
+            self.iterations = b
+            it = b + 1
+            if stop is not None and stop():
+                break
 
 
 def _repair_many(instance, workers):
@@ -635,40 +831,53 @@ def _repair_many(instance, workers):
 
 def run_alns(instance, params: AlnsParams, seed: int, initial: Solution | None = None,
              share: _PoolShare | None = None, global_share: _PoolShare | None = None,
-             worker_id: int = 0, rng=None):
-    """Single trajectory (alns.py:536-640); returns (best Solution, AlnsStats)."""
+             worker_id: int = 0, rng=None, engine: str = "device"):
+    """Single trajectory (alns.py:536-640); returns (best Solution, AlnsStats).
+    engine "device": the whole loop body runs in vrp_alns_iterate; "host":
+    destroy/acceptance on the host, repair + scoring batched on the device."""
     w = _Worker(instance, params, seed, initial, share, global_share, worker_id, rng=rng)
-    for it in range(1, params.max_iter + 1):
-        w.propose(it)
-        (cand, z, failed), = _repair_many(instance, [w])
-        w.conclude(it, cand, z, failed)
+    _drive([w], engine)
     return w.finish()
 
 
-def run_pool(instance, params: AlnsParams, pool_size: int, seed: int,
-             initial: Solution | None = None):
-    """pool_size workers with derived seeds (alns.py:643-685), advanced in
-    lockstep so each iteration is one batched repair + one batched scoring.
-    Workers offer/poll their pool's incumbent in worker order (deterministic;
-    the reference's threads interleave nondeterministically)."""
-    if pool_size < 1:
-        raise ValueError("pool_size must be >= 1")
-    if pool_size == 1:
-        best, stats = run_alns(instance, params, worker_seed(seed, 0), initial=initial)
-        return best, {"workers": 1, "pools": 1, "best_makespan": evaluate(instance, best).makespan,
-                      "worker_stats": [stats]}
-    n_pools = (pool_size + params.workers_per_pool - 1) // params.workers_per_pool
-    pools = [_PoolShare() for _ in range(n_pools)]
-    global_share = _PoolShare() if n_pools > 1 else None
-    workers = [_Worker(instance, params, worker_seed(seed, i), initial,
-                       pools[i // params.workers_per_pool], global_share, i)
-               for i in range(pool_size)]
+def _drive(workers, engine: str):
+    if engine == "device":
+        if workers[0].params.max_iter:
+            _DeviceWorkers(workers[0].instance, workers[0].params, workers).drive()
+        return
+    if engine != "host":
+        raise ValueError(f"unknown engine {engine!r}")
+    instance, params = workers[0].instance, workers[0].params
     for it in range(1, params.max_iter + 1):
         for w in workers:
             w.propose(it)
         results = _repair_many(instance, workers)
         for w, (cand, z, failed) in zip(workers, results):
             w.conclude(it, cand, z, failed)
+
+
+def run_pool(instance, params: AlnsParams, pool_size: int, seed: int,
+             initial: Solution | None = None, engine: str = "device"):
+    """pool_size workers with derived seeds (alns.py:643-685).  Workers offer
+    and poll their pool's incumbent in worker order (deterministic; the
+    reference's threads interleave nondeterministically).  engine "device":
+    one warp per worker inside vrp_alns_iterate; "host": lockstep iterations
+    with one batched repair + one batched scoring launch each."""
+    if pool_size < 1:
+        raise ValueError("pool_size must be >= 1")
+    if pool_size == 1:
+        best, stats = run_alns(instance, params, worker_seed(seed, 0), initial=initial, engine=engine)
+        return best, {"workers": 1, "pools": 1, "best_makespan": evaluate(instance, best).makespan,
+                      "worker_stats": [stats]}
+    if initial is None:
+        initial = construct_initial(instance)
+    n_pools = (pool_size + params.workers_per_pool - 1) // params.workers_per_pool
+    pools = [_PoolShare() for _ in range(n_pools)]
+    global_share = _PoolShare() if n_pools > 1 else None
+    workers = [_Worker(instance, params, worker_seed(seed, i), initial,
+                       pools[i // params.workers_per_pool], global_share, i)
+               for i in range(pool_size)]
+    _drive(workers, engine)
     results = [w.finish() for w in workers]
     best, z_best = None, math.inf
     for sol, _ in results:

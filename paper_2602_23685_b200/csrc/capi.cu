@@ -219,4 +219,42 @@ int vrp_repair_batch(vrp_instance_t h, const int32_t *partial_ops, int64_t parti
                          "vrp_repair_batch");
 }
 
+int vrp_alns_iterate(vrp_instance_t h, const vrp_alns_params *params, vrp_alns_worker *workers,
+                     int32_t nw, int32_t *cur_ops, int32_t *cur_lens, int32_t *best_ops,
+                     int32_t *best_lens, const int32_t *q_draws, int64_t q_stride, int64_t it_begin,
+                     int64_t it_end, int32_t *trace_it, double *trace_z, int64_t trace_cap,
+                     int32_t *rows_it, double *rows_val, int64_t rows_cap, void *stream) {
+    if (!h) return fail(VRP_EINVAL, "null instance%s");
+    if (!params) return fail(VRP_EINVAL, "vrp_alns_iterate: null params%s");
+    if (nw < 0 || it_begin < 1) return fail(VRP_EINVAL, "vrp_alns_iterate: bad worker count / iteration%s");
+    if (nw == 0 || it_end < it_begin) return 0;
+    if (!workers || !cur_ops || !cur_lens || !best_ops || !best_lens || !q_draws || !trace_it ||
+        !trace_z || !rows_it || !rows_val)
+        return fail(VRP_EINVAL, "vrp_alns_iterate: null buffer%s");
+    if (q_stride < it_end) return fail(VRP_EINVAL, "vrp_alns_iterate: q_stride < it_end%s");
+    if (params->weight_interval < 1) return fail(VRP_EINVAL, "vrp_alns_iterate: weight_interval < 1%s");
+    return launch_result(launch_alns(h->dev, *params, workers, nw, cur_ops, cur_lens, best_ops, best_lens,
+                                     q_draws, q_stride, it_begin, it_end, trace_it, trace_z, trace_cap,
+                                     rows_it, rows_val, rows_cap, static_cast<cudaStream_t>(stream)),
+                         "vrp_alns_iterate");
+}
+
+int vrp_destroy_batch(vrp_instance_t h, const int32_t *ops, int64_t op_stride, const int32_t *lens,
+                      const int32_t *opcode, const int32_t *q, int32_t q_min, vrp_philox *states,
+                      int32_t *out_ops, int64_t out_stride, int32_t *out_lens, int32_t *removed,
+                      int64_t removed_stride, int32_t *nremoved, int64_t N, void *stream) {
+    if (!h) return fail(VRP_EINVAL, "null instance%s");
+    if (N < 0) return fail(VRP_EINVAL, "vrp_destroy_batch: N < 0%s");
+    if (N == 0) return 0;
+    if (!ops || !lens || !opcode || !q || !states || !out_ops || !out_lens || !removed || !nremoved)
+        return fail(VRP_EINVAL, "vrp_destroy_batch: null buffer%s");
+    const int64_t n = h->dev.n;
+    if (op_stride < 2 * n || out_stride < 2 * n || removed_stride < n)
+        return fail(VRP_EINVAL, "vrp_destroy_batch: stride too small%s");
+    return launch_result(launch_destroy(h->dev, ops, op_stride, lens, opcode, q, q_min, states, out_ops,
+                                        out_stride, out_lens, removed, removed_stride, nremoved, N,
+                                        static_cast<cudaStream_t>(stream)),
+                         "vrp_destroy_batch");
+}
+
 }  // extern "C"

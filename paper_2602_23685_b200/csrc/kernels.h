@@ -33,3 +33,15 @@ int launch_repair(const DevInstance &I, const int32_t *pops, int64_t pstride, co
                   const int32_t *removed, int64_t rstride, const int32_t *nremoved,
                   const int32_t *regret_k, vrp_philox *states, int32_t *out_ops, int64_t ostride,
                   int32_t *out_lens, int32_t *status, int64_t N, cudaStream_t stream);
+
+// alns_step.cu (K6 + device ALNS iterations)
+size_t alns_scratch_bytes(int n, int m);
+int launch_alns(const DevInstance &I, const vrp_alns_params &P, vrp_alns_worker *workers, int32_t nw,
+                int32_t *cur_ops, int32_t *cur_lens, int32_t *best_ops, int32_t *best_lens,
+                const int32_t *q_draws, int64_t q_stride, int64_t it_begin, int64_t it_end,
+                int32_t *trace_it, double *trace_z, int64_t trace_cap, int32_t *rows_it,
+                double *rows_val, int64_t rows_cap, cudaStream_t stream);
+int launch_destroy(const DevInstance &I, const int32_t *ops, int64_t stride, const int32_t *lens,
+                   const int32_t *opcode, const int32_t *q, int32_t q_min, vrp_philox *states,
+                   int32_t *out_ops, int64_t ostride, int32_t *out_lens, int32_t *removed,
+                   int64_t rstride, int32_t *nremoved, int64_t N, cudaStream_t stream);

@@ -262,3 +262,66 @@ def repair_batch(instance, partial_ops, partial_lens, removed, nremoved, regret_
                                      N.ptr(out["status"]), Nn, N.stream_handle(stream)),
             "vrp_repair_batch")
     return out
+
+
+DESTROY_CODES = {"random": 0, "worst": 1, "shaw": 2, "cluster": 3, "route": 4, "critical_path": 5}
+
+
+def destroy_batch(instance, ops, lens, operators, q, q_min, states, stream=None):
+    """K6: destroy + remove_customers on N complete solutions (device tensors).
+
+    ops [N, >=2n] int32, lens [N, m] int32, operators [N] int32 (DESTROY_CODES),
+    q [N] int32, states uint8 [N, 96] device generators (advanced in place).
+    Returns dict(ops [N, 2n] partials, lens [N, m], removed [N, n] (sorted,
+    -padded after nremoved), nremoved [N])."""
+    di = device_instance(instance)
+    o = _cuda(ops, torch.int32)
+    ln = _cuda(lens, torch.int32)
+    op = _cuda(operators, torch.int32)
+    qq = _cuda(q, torch.int32)
+    Nn = o.shape[0]
+    dev = o.device
+    if states.dtype != torch.uint8 or states.shape[-1] != 96 or states.shape[0] != Nn:
+        raise ValueError("states must be uint8 [N, 96] device generator states")
+    out = {"ops": torch.empty((Nn, 2 * di.n), dtype=torch.int32, device=dev),
+           "lens": torch.empty((Nn, di.m), dtype=torch.int32, device=dev),
+           "removed": torch.zeros((Nn, di.n), dtype=torch.int32, device=dev),
+           "nremoved": torch.empty(Nn, dtype=torch.int32, device=dev)}
+    N.check(N.lib().vrp_destroy_batch(di.handle, N.ptr(o), row_stride(o), N.ptr(ln), N.ptr(op), N.ptr(qq),
+                                      int(q_min), N.ptr(states), N.ptr(out["ops"]), 2 * di.n,
+                                      N.ptr(out["lens"]), N.ptr(out["removed"]), di.n,
+                                      N.ptr(out["nremoved"]), Nn, N.stream_handle(stream)),
+            "vrp_destroy_batch")
+    return out
+
+
+# vrp_alns_worker / vrp_alns_params (include/vrp_rpd.h), field for field
+ALNS_WORKER_DTYPE = np.dtype([
+    ("rng", np.uint8, 96), ("z", "<f8"), ("z_best", "<f8"), ("temperature", "<f8"), ("t_init", "<f8"),
+    ("weights", "<f8", 10), ("scores", "<f8", 10), ("attempts", "<i8", 10),
+    ("stagnation", "<i8"), ("accepted", "<i8"), ("rejected", "<i8"), ("reheats", "<i8"),
+    ("best_it", "<i8"), ("n_trace", "<i4"), ("n_rows", "<i4")])
+
+
+class AlnsParamsC(C.Structure):
+    _fields_ = [("t0", C.c_double), ("alpha", C.c_double), ("reheat_factor", C.c_double),
+                ("reaction", C.c_double), ("sigma1", C.c_double), ("sigma2", C.c_double),
+                ("sigma3", C.c_double), ("min_weight", C.c_double),
+                ("stagnation_threshold", C.c_int64), ("weight_interval", C.c_int64),
+                ("q_min", C.c_int32), ("reserved", C.c_int32)]
+
+
+def alns_iterate(instance, params: AlnsParamsC, workers, cur_ops, cur_lens, best_ops, best_lens,
+                 q_draws, it_begin: int, it_end: int, trace_it, trace_z, rows_it, rows_val,
+                 stream=None):
+    """Device-resident ALNS iterations it_begin..it_end for every worker
+    (vrp_alns_iterate).  All tensors live on the device and are updated in place:
+    workers uint8 [W, 416], cur/best ops [W, 2n] + lens [W, m], q_draws [W, >=it_end],
+    trace_it/trace_z [W, cap], rows_it [W, rcap], rows_val [W, rcap, 12]."""
+    di = device_instance(instance)
+    W = workers.shape[0]
+    N.check(N.lib().vrp_alns_iterate(
+        di.handle, C.byref(params), N.ptr(workers), W, N.ptr(cur_ops), N.ptr(cur_lens),
+        N.ptr(best_ops), N.ptr(best_lens), N.ptr(q_draws), row_stride(q_draws), int(it_begin), int(it_end),
+        N.ptr(trace_it), N.ptr(trace_z), trace_it.shape[1], N.ptr(rows_it), N.ptr(rows_val),
+        rows_it.shape[1], N.stream_handle(stream)), "vrp_alns_iterate")

@@ -37,12 +37,12 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.5, pool_
                         brkga_params: B.BrkgaParams | None = None, seed: int = 0,
                         initial: Solution | None = None):
     """Best makespan found within a wall-clock budget (the BASELINE metric's
-    'best makespan at fixed time'): ALNS worker batches (one K5 + one K1 launch
-    per iteration) for ``alns_share`` of the budget, then BRKGA generations
+    'best makespan at fixed time'): device-resident ALNS workers (one warp
+    each, vrp_alns_iterate) for ``alns_share`` of the budget, then BRKGA generations
     warm-started from the ALNS incumbent for the rest.  Returns
     (best Solution, best makespan, trace [(seconds, best)])."""
     t0 = time.perf_counter()
-    alns_params = alns_params or A.AlnsParams(max_iter=10**9)
+    alns_params = alns_params or A.AlnsParams(max_iter=200_000)
     brkga_params = brkga_params or B.BrkgaParams(population=4096, generations=1)
     trace = []
     init = initial if initial is not None else A.construct_initial(instance, seed)
@@ -50,17 +50,17 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.5, pool_
                for i in range(pool_size)]
     best = min(((w.z_best, w.best) for w in workers), key=lambda x: x[0])
     trace.append((time.perf_counter() - t0, best[0]))
-    it = 0
-    while time.perf_counter() - t0 < alns_share * seconds:
-        it += 1
-        for w in workers:
-            w.propose(it)
-        for w, (cand, z, failed) in zip(workers, A._repair_many(instance, workers)):
-            w.conclude(it, cand, z, failed)
-        cur = min(((w.z_best, w.best) for w in workers), key=lambda x: x[0])
-        if cur[0] < best[0]:
-            best = cur
+
+    def stop():
+        nonlocal best
+        w = min(workers, key=lambda w: w.z_best)
+        if w.z_best < best[0]:
+            best = (w.z_best, w.best)
             trace.append((time.perf_counter() - t0, best[0]))
+        return time.perf_counter() - t0 >= alns_share * seconds
+
+    if alns_params.max_iter:
+        A._DeviceWorkers(instance, alns_params, workers).drive(stop=stop, max_stretch=25)
     incumbent = best[1]
     rng = R.philox_generator(A.worker_seed(seed, 7001), R.BRKGA_STREAM)
     pop = B.warm_start_population(instance, incumbent, brkga_params, rng)

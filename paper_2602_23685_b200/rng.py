@@ -44,7 +44,8 @@ def as_philox(rng, stream: int = 0) -> np.random.Generator:
     return np.random.Generator(np.random.Philox(key=(int(words[0]), int(words[1]) ^ stream)))
 
 
-def state_to_device(gen: np.random.Generator, device=None) -> torch.Tensor:
+def state_bytes(gen: np.random.Generator) -> np.ndarray:
+    """The vrp_philox struct (uint8[96]) of a Generator(Philox)."""
     st = gen.bit_generator.state
     if st["bit_generator"] != "Philox":
         raise TypeError("device RNG needs Generator(Philox)")
@@ -55,12 +56,12 @@ def state_to_device(gen: np.random.Generator, device=None) -> torch.Tensor:
     rec["buffer_pos"][0] = int(st["buffer_pos"])
     rec["has_uint32"][0] = int(st["has_uint32"])
     rec["uinteger"][0] = int(st["uinteger"])
-    t = torch.from_numpy(rec.view(np.uint8).copy())
-    return t.to(device if device is not None else torch.device("cuda", torch.cuda.current_device()))
+    return rec.view(np.uint8).copy()
 
 
-def state_from_device(gen: np.random.Generator, t: torch.Tensor) -> None:
-    rec = t.detach().cpu().numpy().view(_DTYPE)[0]
+def set_state_bytes(gen: np.random.Generator, raw) -> None:
+    """Load a vrp_philox struct (uint8[96]) into a Generator(Philox)."""
+    rec = np.ascontiguousarray(raw, dtype=np.uint8).reshape(-1).view(_DTYPE)[0]
     gen.bit_generator.state = {
         "bit_generator": "Philox",
         "state": {"counter": np.array(rec["ctr"], dtype=np.uint64),
@@ -70,3 +71,12 @@ def state_from_device(gen: np.random.Generator, t: torch.Tensor) -> None:
         "has_uint32": int(rec["has_uint32"]),
         "uinteger": int(rec["uinteger"]),
     }
+
+
+def state_to_device(gen: np.random.Generator, device=None) -> torch.Tensor:
+    t = torch.from_numpy(state_bytes(gen))
+    return t.to(device if device is not None else torch.device("cuda", torch.cuda.current_device()))
+
+
+def state_from_device(gen: np.random.Generator, t: torch.Tensor) -> None:
+    set_state_bytes(gen, t.detach().cpu().numpy())

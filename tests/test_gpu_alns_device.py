@@ -1,0 +1,135 @@
+"""Device-resident ALNS (csrc/alns_step.cu): K6 destroy against the
+reference's destroy goldens and the host destroy at scale, and whole
+vrp_alns_iterate trajectories against the reference's run_alns goldens and
+the host engine (pools included)."""
+import numpy as np
+import pytest
+import torch
+
+import inputs as I
+from conftest import config_instance
+from paper_2602_23685_b200 import alns as A
+from paper_2602_23685_b200 import device as DV
+from paper_2602_23685_b200 import rng as R
+from paper_2602_23685_b200.schedule import Solution
+
+pytestmark = pytest.mark.gpu
+CID = {"gr17": 1, "eil51": 2, "kroA100": 3, "a280": 4, "dsj1000": 5}
+
+
+def _destroy_dev(inst, sols, ops_names, qs, gens):
+    n = inst.n
+    arrs = [s.to_arrays(n) for s in sols]
+    ops = np.stack([o[:2 * n] for o, _ in arrs])
+    lens = np.stack([l for _, l in arrs])
+    states = torch.from_numpy(np.stack([R.state_bytes(g) for g in gens])).cuda()
+    codes = np.array([DV.DESTROY_CODES[o] for o in ops_names], np.int32)
+    r = DV.destroy_batch(inst, torch.from_numpy(ops).cuda(), torch.from_numpy(lens).cuda(),
+                         torch.from_numpy(codes).cuda(), torch.from_numpy(np.asarray(qs, np.int32)).cuda(),
+                         min(A.removal_bounds(n)[0], n), states)
+    st = states.cpu().numpy()
+    for g, raw in zip(gens, st):
+        R.set_state_bytes(g, raw)
+    nr = r["nremoved"].cpu().numpy()
+    rem = r["removed"].cpu().numpy()
+    return r["ops"].cpu().numpy(), r["lens"].cpu().numpy(), [list(rem[i, :nr[i]]) for i in range(len(sols))]
+
+
+def test_destroy_kernel_matches_reference_goldens(golden, golden_meta):
+    by_key = {}
+    for i, rec in enumerate(golden_meta["destroys"]):
+        by_key.setdefault(rec["key"], []).append(i)
+    for key, idx in by_key.items():
+        inst = config_instance(key)
+        recs = [golden_meta["destroys"][i] for i in idx]
+        sols = [Solution.from_arrays(golden[f"{key}/dec_ops"][r["case"]], golden[f"{key}/dec_lens"][r["case"]])
+                for r in recs]
+        gens = [I.philox(41, CID[key], r["case"]) for r in recs]
+        o, l, rem = _destroy_dev(inst, sols, [r["operator"] for r in recs], [r["q"] for r in recs], gens)
+        for j, (i, r) in enumerate(zip(idx, recs)):
+            msg = f"{key} {r['operator']} case {r['case']}"
+            assert rem[j] == list(golden[f"destroy/{i}/removed"]), msg
+            np.testing.assert_array_equal(l[j], golden[f"destroy/{i}/lens"], err_msg=msg)
+            np.testing.assert_array_equal(o[j], golden[f"destroy/{i}/ops"], err_msg=msg)
+            st = gens[j].bit_generator.state
+            assert [int(x) for x in st["state"]["counter"]] == r["final_counter"], msg
+            assert int(st["buffer_pos"]) == r["final_buffer_pos"], msg
+            assert int(st["has_uint32"]) == r["final_has_uint32"], msg
+
+
+@pytest.mark.parametrize("key,count", [("gr17", 48), ("eil51", 48), ("kroA100", 36), ("a280", 18),
+                                       ("dsj1000", 6)])
+def test_destroy_kernel_vs_host_at_scale(key, count, golden):
+    """Fresh solutions and seeds; every operator; q across [q_min, q_max]."""
+    inst = config_instance(key)
+    n = inst.n
+    base = golden[f"{key}/dec_ops"], golden[f"{key}/dec_lens"]
+    qmin, qmax = A.removal_bounds(n)
+    sols, names, qs = [], [], []
+    for i in range(count):
+        j = i % base[0].shape[0]
+        sols.append(Solution.from_arrays(base[0][j], base[1][j]))
+        names.append(A.DESTROY_OPERATORS[i % 6])
+        qs.append(min(n, qmin + (i * 7) % (qmax - qmin + 1) + (i % 5 == 4) * 3))
+    g_dev = [I.philox(71, CID[key], i) for i in range(count)]
+    o, l, rem = _destroy_dev(inst, sols, names, qs, g_dev)
+    for i in range(count):
+        g = I.philox(71, CID[key], i)
+        partial, removed = A.destroy(inst, sols[i], names[i], qs[i], g)
+        po, pl = partial.to_arrays(n)
+        assert rem[i] == removed, (names[i], i)
+        np.testing.assert_array_equal(l[i], pl, err_msg=f"{names[i]} {i}")
+        np.testing.assert_array_equal(o[i], po[:2 * n], err_msg=f"{names[i]} {i}")
+        assert np.array_equal(R.state_bytes(g), R.state_bytes(g_dev[i])), (names[i], i)
+
+
+def test_device_run_alns_matches_reference(golden, golden_meta):
+    for j, run in enumerate(golden_meta["alns_runs"]):
+        inst = config_instance(run["key"])
+        params = A.AlnsParams(max_iter=run["iters"], **run["extra"])
+        initial = None
+        if run["init"]:
+            initial = Solution.from_arrays(golden[f"{run['key']}/dec_ops"][0],
+                                           golden[f"{run['key']}/dec_lens"][0])
+        best, st = A.run_alns(inst, params, seed=run["seed"], initial=initial, engine="device")
+        ops, lens = best.to_arrays(inst.n)
+        np.testing.assert_array_equal(ops, golden[f"alns/{j}/ops"], err_msg=str(j))
+        np.testing.assert_array_equal(lens, golden[f"alns/{j}/lens"])
+        assert [list(x) for x in st.best_trace] == [list(x) for x in run["best_trace"]], j
+        assert st.accepted == run["accepted"] and st.rejected_candidates == run["rejected"], j
+        assert st.reheats == run["reheats"]
+        assert st.final_temperature == run["final_temperature"]
+        assert st.attempts == run["attempts"]
+        assert st.weight_rows == run["weight_rows"], j
+
+
+def _same_stats(a, b):
+    assert a.best_trace == b.best_trace
+    assert a.accepted == b.accepted and a.rejected_candidates == b.rejected_candidates
+    assert a.reheats == b.reheats and a.final_temperature == b.final_temperature
+    assert a.attempts == b.attempts and a.weight_rows == b.weight_rows
+
+
+@pytest.mark.parametrize("key,iters,seed", [("eil51", 450, 3), ("kroA100", 120, 4), ("a280", 25, 5)])
+def test_device_engine_equals_host_engine(key, iters, seed):
+    """Longer single trajectories (local search at 200/400 included)."""
+    inst = config_instance(key)
+    params = A.AlnsParams(max_iter=iters, weight_interval=40, stagnation_threshold=30, t0=0.05)
+    initial = A.construct_initial(inst)
+    b1, s1 = A.run_alns(inst, params, seed=seed, initial=initial, engine="device")
+    b2, s2 = A.run_alns(inst, params, seed=seed, initial=initial, engine="host")
+    assert b1 == b2
+    _same_stats(s1, s2)
+
+
+def test_device_pool_equals_host_pool():
+    """Pools with share polling / merging at stretch boundaries."""
+    inst = config_instance("eil51")
+    params = A.AlnsParams(max_iter=60, best_check_interval=7, pool_sync_interval=5, workers_per_pool=3,
+                          pickup_reposition_interval=20, cross_agent_interval=50)
+    initial = A.construct_initial(inst)
+    b1, i1 = A.run_pool(inst, params, pool_size=8, seed=21, initial=initial, engine="device")
+    b2, i2 = A.run_pool(inst, params, pool_size=8, seed=21, initial=initial, engine="host")
+    assert b1 == b2 and i1["best_makespan"] == i2["best_makespan"]
+    for a, b in zip(i1["worker_stats"], i2["worker_stats"]):
+        _same_stats(a, b)
