@@ -144,7 +144,8 @@ def extra_rates(device, ops, lens, decode_ms, n_dec):
     """Secondary §8 throughputs on this GPU (not the headline): K3 decodes/s
     (the bench set-up, CUDA-event timed), BRKGA generations/s at paper scale
     (N_p = 30,000) on the a280 island config and dsj1000, ALNS repairs/s
-    (K5, 1024 instances) on the eil51 ALNS config."""
+    (K5, 1024 instances) and device-resident ALNS iterations/s on the eil51
+    ALNS config."""
     import torch
     from oracle import oracle as O
     import inputs as I
@@ -180,6 +181,19 @@ def extra_rates(device, ops, lens, decode_ms, n_dec):
     INS.reinsert_batch(inst, parts, plens, rem, rks, [I.philox(9, i) for i in range(cnt)])
     torch.cuda.synchronize()
     out["alns_repairs_per_s_eil51"] = cnt / (time.perf_counter() - t0)
+    # device-resident ALNS (vrp_alns_iterate): whole iterations (destroy, repair,
+    # exact scoring, SA) per second, 1184 workers = 8 per SM, local search off
+    from paper_2602_23685_b200 import alns as A
+    init = A.construct_initial(inst)
+    prm = A.AlnsParams(max_iter=100, pickup_reposition_interval=10**9, cross_agent_interval=10**9)
+    ws = [A._Worker(inst, prm, A.worker_seed(3, i), init, None, None, i) for i in range(1184)]
+    dw = A._DeviceWorkers(inst, prm, ws)
+    dw.run(1, 5)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    dw.run(6, 100)
+    torch.cuda.synchronize()
+    out["alns_iterations_per_s_eil51_1184_workers"] = 1184 * 95 / (time.perf_counter() - t0)
     return {k: round(v, 2) for k, v in out.items()}
 
 
