@@ -762,8 +762,9 @@ class _DeviceWorkers:
         self.rec = rec.copy()
         return improved
 
-    def drive(self, stop=None, max_stretch: int | None = None):
-        """Run to max_iter (or until ``stop()`` is true at a stretch end)."""
+    def drive(self, stop=None, max_stretch: int | None = None, on_boundary=None):
+        """Run to max_iter (or until ``stop()`` is true at a stretch end);
+        ``on_boundary(b)`` runs after every worker's post(b)."""
         p, workers = self.params, self.workers
         pooled = workers[0].share is not None
         it = 1
@@ -789,6 +790,8 @@ class _DeviceWorkers:
                 self.run(it, b)
                 for w in workers:
                     w.post(b)
+            if on_boundary is not None:
+                on_boundary(b)
             self.push()
             self.iterations = b
             it = b + 1
@@ -840,10 +843,10 @@ def run_alns(instance, params: AlnsParams, seed: int, initial: Solution | None =
     return w.finish()
 
 
-def _drive(workers, engine: str):
+def _drive(workers, engine: str, on_boundary=None):
     if engine == "device":
         if workers[0].params.max_iter:
-            _DeviceWorkers(workers[0].instance, workers[0].params, workers).drive()
+            _DeviceWorkers(workers[0].instance, workers[0].params, workers).drive(on_boundary=on_boundary)
         return
     if engine != "host":
         raise ValueError(f"unknown engine {engine!r}")
@@ -854,6 +857,8 @@ def _drive(workers, engine: str):
         results = _repair_many(instance, workers)
         for w, (cand, z, failed) in zip(workers, results):
             w.conclude(it, cand, z, failed)
+        if on_boundary is not None and workers[0].host_step(it):
+            on_boundary(it)
 
 
 def run_pool(instance, params: AlnsParams, pool_size: int, seed: int,
@@ -889,3 +894,84 @@ def run_pool(instance, params: AlnsParams, pool_size: int, seed: int,
             best, z_best = pool.best_sol, pool.best_z
     return best, {"workers": pool_size, "pools": n_pools, "best_makespan": z_best,
                   "worker_stats": [st for _, st in results]}
+
+
+# --------------------------------------------------------------------------
+# multi-GPU pools: pools sharded over ranks, the global share
+# kept consistent by a min-all-reduce + broadcast at every pool_sync boundary
+# --------------------------------------------------------------------------
+
+def _dist_world(group):
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized():
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def sync_pool_share(instance, share: _PoolShare, group=None) -> None:
+    """Make ``share`` the best over all ranks: min-all-reduce of its makespan,
+    the lowest rank among equals wins, its routes are broadcast (2n + m int32).
+    The result is the same on every rank (src = None, as after merge())."""
+    import torch
+    import torch.distributed as dist
+    rank, world = _dist_world(group)
+    if world < 2:
+        return
+    dev = (torch.device("cuda", torch.cuda.current_device())
+           if dist.get_backend(group) == "nccl" else torch.device("cpu"))
+    z = torch.tensor([share.best_z], dtype=torch.float64, device=dev)
+    dist.all_reduce(z, op=dist.ReduceOp.MIN, group=group)
+    zmin = float(z.item())
+    if zmin == math.inf:
+        return
+    cand = torch.tensor([rank if share.best_z == zmin else world], dtype=torch.int64, device=dev)
+    dist.all_reduce(cand, op=dist.ReduceOp.MIN, group=group)
+    winner = int(cand.item())
+    n, m = instance.n, instance.m
+    buf = torch.zeros(2 * n + m, dtype=torch.int32, device=dev)
+    if rank == winner:
+        o, l = share.best_sol.to_arrays(n)
+        buf[:2 * n] = torch.from_numpy(o[:2 * n])
+        buf[2 * n:] = torch.from_numpy(l)
+    src = dist.get_global_rank(group, winner) if group is not None else winner
+    dist.broadcast(buf, src=src, group=group)
+    arr = buf.cpu().numpy()
+    share.best_z, share.src = zmin, None
+    share.best_sol = Solution.from_arrays(arr[:2 * n], arr[2 * n:])
+
+
+def run_pool_distributed(instance, params: AlnsParams, pool_size: int, seed: int,
+                         initial: Solution | None = None, group=None, engine: str = "device"):
+    """run_pool with its pools sharded over the ranks of ``group`` (pool p on
+    rank p % world).  Workers keep their global ids and seeds; every rank's
+    copy of the global share is re-synchronised (sync_pool_share) after each
+    pool_sync_interval boundary, so a pool merges with the best of all GPUs
+    as of the previous boundary.  Every rank returns the same result."""
+    rank, world = _dist_world(group)
+    wpp = params.workers_per_pool
+    n_pools = (pool_size + wpp - 1) // wpp
+    if world > n_pools:
+        raise ValueError(f"{world} ranks need at least {world} pools (pool_size / workers_per_pool)")
+    if initial is None:
+        initial = construct_initial(instance)
+    pools = {p: _PoolShare() for p in range(n_pools) if p % world == rank}
+    global_share = _PoolShare() if (n_pools > 1 or world > 1) else None
+    workers = [_Worker(instance, params, worker_seed(seed, i), initial, pools[i // wpp], global_share, i)
+               for i in range(pool_size) if (i // wpp) % world == rank]
+
+    def boundary(b):
+        if global_share is not None and b % params.pool_sync_interval == 0:
+            sync_pool_share(instance, global_share, group)
+
+    _drive(workers, engine, on_boundary=boundary)
+    results = [w.finish() for w in workers]
+    final = _PoolShare()
+    for sol, _ in results:
+        final.offer(-1, evaluate(instance, sol).makespan, sol)
+    for pool in pools.values():
+        if pool.best_sol is not None:
+            final.offer(-1, pool.best_z, pool.best_sol)
+    sync_pool_share(instance, final, group)
+    return final.best_sol, {"workers": pool_size, "pools": n_pools, "ranks": world,
+                            "local_workers": len(workers), "best_makespan": final.best_z,
+                            "worker_stats": [st for _, st in results]}
