@@ -159,6 +159,25 @@ int vrp_destroy_batch(vrp_instance_t h, const int32_t *ops, int64_t op_stride, c
                       int32_t *out_ops, int64_t out_stride, int32_t *out_lens, int32_t *removed,
                       int64_t removed_stride, int32_t *nremoved, int64_t N, void *stream);
 
+/* Local-search neighbourhoods (alns.py:416-487 pickup_repositioning /
+ * cross_agent_relocation) materialised as a candidate batch for
+ * vrp_makespan_batch (K2 estimate, K1 verify).  Candidates are numbered in the
+ * reference's generation order:
+ *   kind 0 (pickup move): entries[e] = {worker, v, i, fi, 0} -- the pickup at
+ *     position i of vehicle v (flat index fi of the worker's solution) is
+ *     removed and re-inserted at every (w, g) of the reduced solution except
+ *     (v, i): 2n + m - 2 candidates per entry, index = e * (2n+m-2) + j
+ *   kind 1 (cross move): entries[e] = {worker, c, w, f1, f2} -- customer c
+ *     (flat op positions f1 < f2) is stripped and re-inserted as D at gd, P at
+ *     gp (0 <= gd < gp <= L_w + 1) on vehicle w: entry_start[e] = first index
+ *   base_ops[W][2n], base_lens[W][m]: the workers' solutions (DEVICE)
+ *   index_list (nullable): explicit candidate indices; else first .. first+count-1
+ *   out_ops[count][2n] (op_bytes 2 or 4), out_lens[count][m] */
+int vrp_ls_build(vrp_instance_t h, int32_t kind, const int32_t *base_ops, const int32_t *base_lens,
+                 const int32_t *entries, const int64_t *entry_start, int64_t n_entries,
+                 const int64_t *index_list, int64_t first, int64_t count, void *out_ops,
+                 int32_t op_bytes, int32_t *out_lens, void *stream);
+
 /* One ALNS worker (alns.py:536-640 run_alns locals), DEVICE-resident.
  * weights/scores/attempts are indexed in the reference's operator order:
  * random, worst, shaw, cluster, route, critical_path, greedy, regret2,

@@ -352,10 +352,10 @@ def _estimate_filter(instance, cand_ops, cand_lens, z):
             if s == 0 and e < z - 1e-9]
 
 
-def pickup_repositioning(instance, solution: Solution) -> Solution:
-    """Move pickups off (near-)bottleneck vehicles; <= 3 improvement passes
-    (alns.py:416-450).  Candidates are built as flat op arrays, estimated in
-    one K2 launch, the best ten verified in one K1 launch."""
+def _pickup_repositioning_host(instance, solution: Solution) -> Solution:
+    """Host-built neighbourhood variant of pickup_repositioning (candidates as
+    numpy op arrays, scored by K2/K1) -- kept as the cross-check of the
+    device-built batch path (tests/test_gpu_localsearch.py)."""
     tours = [list(t) for t in solution.tours]
     m = instance.m
     for _ in range(3):
@@ -391,8 +391,8 @@ def pickup_repositioning(instance, solution: Solution) -> Solution:
     return Solution.from_lists(tours)
 
 
-def cross_agent_relocation(instance, solution: Solution) -> Solution:
-    """Move whole customers off the bottleneck route; <= 3 passes (alns.py:453-487)."""
+def _cross_agent_relocation_host(instance, solution: Solution) -> Solution:
+    """Host-built neighbourhood variant of cross_agent_relocation (cross-check)."""
     if instance.m == 1:
         return solution
     tours = [list(t) for t in solution.tours]
@@ -429,6 +429,33 @@ def cross_agent_relocation(instance, solution: Solution) -> Solution:
             break
         tours = new_tours
     return Solution.from_lists(tours)
+
+
+def _ls_batch(instance, kind, sols):
+    from . import localsearch as LS
+    n = instance.n
+    arrs = [s.to_arrays(n) for s in sols]
+    ops = np.stack([o[:2 * n] for o, _ in arrs])
+    lens = np.stack([l for _, l in arrs])
+    fn = LS.pickup_repositioning_batch if kind == 0 else LS.cross_agent_relocation_batch
+    o, l, z = fn(instance, ops, lens)
+    o, l = o.cpu().numpy(), l.cpu().numpy()
+    return [Solution.from_arrays(o[i], l[i]) for i in range(len(sols))], z
+
+
+def pickup_repositioning(instance, solution: Solution) -> Solution:
+    """Move pickups off (near-)bottleneck vehicles; <= 3 improvement passes
+    (alns.py:416-450).  The neighbourhood is built on the device and estimated
+    by K2, the best ten verified by K1 (localsearch.py)."""
+    return _ls_batch(instance, 0, [solution])[0][0]
+
+
+def cross_agent_relocation(instance, solution: Solution) -> Solution:
+    """Move whole customers off the bottleneck route; <= 3 passes
+    (alns.py:453-487), device-built neighbourhood (localsearch.py)."""
+    if instance.m == 1:
+        return solution
+    return _ls_batch(instance, 1, [solution])[0][0]
 
 
 def construct_initial(instance, seed: int = 0) -> Solution:
@@ -605,16 +632,24 @@ class _Worker:
     def post(self, it: int):
         """alns.py:612-640: local search, pool share polling and merging."""
         p, inst = self.params, self.instance
+        cache = getattr(self, "ls_cache", None) or {}
+        self.ls_cache = None
         if it % p.pickup_reposition_interval == 0:
-            improved = pickup_repositioning(inst, self.current)
-            z_new = exact_makespan(inst, improved)
+            if "pickup" in cache:
+                improved, z_new = cache["pickup"]
+            else:
+                improved = pickup_repositioning(inst, self.current)
+                z_new = exact_makespan(inst, improved)
             if z_new < self.z:
                 self.current, self.z = improved, z_new
                 if z_new < self.z_best:
                     self._found_best(improved, z_new, it)
         if it % p.cross_agent_interval == 0:
-            improved = cross_agent_relocation(inst, self.current)
-            z_new = exact_makespan(inst, improved)
+            if "cross" in cache:
+                improved, z_new = cache["cross"]
+            else:
+                improved = cross_agent_relocation(inst, self.current)
+                z_new = exact_makespan(inst, improved)
             if z_new < self.z:
                 self.current, self.z = improved, z_new
                 if z_new < self.z_best:
@@ -762,6 +797,35 @@ class _DeviceWorkers:
         self.rec = rec.copy()
         return improved
 
+    def local_search(self, b: int):
+        """The local-search pair of post(b) for every worker in two batched
+        passes (localsearch.py); results are handed to post() in ls_cache.
+        The cross pass starts from the pickup pass's result exactly when
+        post() will have adopted it (strict improvement)."""
+        from . import localsearch as LS
+        p, ws, inst = self.params, self.workers, self.instance
+        do_p = b % p.pickup_reposition_interval == 0
+        do_c = b % p.cross_agent_interval == 0
+        if not (do_p or do_c):
+            return
+        n = inst.n
+        ops, lens = self.g_cur_ops, self.g_cur_lens
+        for w in ws:
+            w.ls_cache = {}
+        if do_p:
+            o, l, z = LS.pickup_repositioning_batch(inst, ops, lens)
+            on, ln = o.cpu().numpy(), l.cpu().numpy()
+            for i, w in enumerate(ws):
+                w.ls_cache["pickup"] = (Solution.from_arrays(on[i], ln[i]), float(z[i]))
+            adopt = self.torch.from_numpy(np.array([float(z[i]) < w.z for i, w in enumerate(ws)])).to(o.device)
+            ops = self.torch.where(adopt[:, None], o, ops)
+            lens = self.torch.where(adopt[:, None], l, lens)
+        if do_c and inst.m > 1:
+            o, l, z = LS.cross_agent_relocation_batch(inst, ops, lens)
+            on, ln = o.cpu().numpy(), l.cpu().numpy()
+            for i, w in enumerate(ws):
+                w.ls_cache["cross"] = (Solution.from_arrays(on[i], ln[i]), float(z[i]))
+
     def drive(self, stop=None, max_stretch: int | None = None, on_boundary=None):
         """Run to max_iter (or until ``stop()`` is true at a stretch end);
         ``on_boundary(b)`` runs after every worker's post(b)."""
@@ -782,12 +846,14 @@ class _DeviceWorkers:
                         w = workers[i]
                         w.share.offer(w.worker_id, w.z_best, w.best)
                 at_b = set(self.run(b, b))
+                self.local_search(b)
                 for i, w in enumerate(workers):
                     if i in at_b:
                         w.share.offer(w.worker_id, w.z_best, w.best)
                     w.post(b)
             else:
                 self.run(it, b)
+                self.local_search(b)
                 for w in workers:
                     w.post(b)
             if on_boundary is not None:

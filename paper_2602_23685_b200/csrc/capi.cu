@@ -257,4 +257,24 @@ int vrp_destroy_batch(vrp_instance_t h, const int32_t *ops, int64_t op_stride, c
                          "vrp_destroy_batch");
 }
 
+int vrp_ls_build(vrp_instance_t h, int32_t kind, const int32_t *base_ops, const int32_t *base_lens,
+                 const int32_t *entries, const int64_t *entry_start, int64_t n_entries,
+                 const int64_t *index_list, int64_t first, int64_t count, void *out_ops,
+                 int32_t op_bytes, int32_t *out_lens, void *stream) {
+    if (!h) return fail(VRP_EINVAL, "null instance%s");
+    if (kind != 0 && kind != 1) return fail(VRP_EINVAL, "vrp_ls_build: kind must be 0 or 1%s");
+    if (op_bytes != 2 && op_bytes != 4) return fail(VRP_EINVAL, "vrp_ls_build: op_bytes must be 2 or 4%s");
+    if (count < 0 || n_entries < 0) return fail(VRP_EINVAL, "vrp_ls_build: negative count%s");
+    if (count == 0) return 0;
+    if (!base_ops || !base_lens || !entries || !out_ops || !out_lens || (kind == 1 && !entry_start) ||
+        n_entries == 0)
+        return fail(VRP_EINVAL, "vrp_ls_build: null buffer%s");
+    if (op_bytes == 2 && 2 * (int64_t)h->dev.n > 32767)
+        return fail(VRP_EUNSUPPORTED, "vrp_ls_build: int16 ops need 2n <= 32767%s");
+    return launch_result(launch_ls_build(kind, h->dev.n, h->dev.m, base_ops, base_lens, entries, entry_start,
+                                         n_entries, index_list, first, count, out_ops, op_bytes, out_lens,
+                                         static_cast<cudaStream_t>(stream)),
+                         "vrp_ls_build");
+}
+
 }  // extern "C"

@@ -45,3 +45,9 @@ int launch_destroy(const DevInstance &I, const int32_t *ops, int64_t stride, con
                    const int32_t *opcode, const int32_t *q, int32_t q_min, vrp_philox *states,
                    int32_t *out_ops, int64_t ostride, int32_t *out_lens, int32_t *removed,
                    int64_t rstride, int32_t *nremoved, int64_t N, cudaStream_t stream);
+
+// ls.cu (batched local-search candidate builder)
+int launch_ls_build(int kind, int n, int m, const int32_t *base_ops, const int32_t *base_lens,
+                    const int32_t *entries, const int64_t *entry_start, int64_t n_entries,
+                    const int64_t *index_list, int64_t first, int64_t count, void *out_ops, int op_bytes,
+                    int32_t *out_lens, cudaStream_t stream);

@@ -1,0 +1,138 @@
+// ls.cu -- candidate builder for the batched local search (alns.py:416-487,
+// SURVEY §8(f) row 1): pickup_repositioning and cross_agent_relocation
+// neighbourhoods materialised on the device, straight into the int16/int32
+// batch layout that K2 (two_pass_estimate) and K1 (exact_makespan) consume.
+//
+// One warp per candidate.  The move is decoded from the candidate's global
+// index in the reference's generation order, then the 2n ops are written with
+// a branch-free position map (coalesced reads of the L2-resident base
+// solution, coalesced writes):
+//   pickup move  (entry = worker, v, i, fi): drop the pickup at route position
+//       i of vehicle v (flat fi), re-insert it at every (w, g) of the reduced
+//       solution except (v, i): K = 2n + m - 2 candidates per entry
+//   cross move   (entry = worker, c, w, f1, f2): strip customer c's two ops
+//       (flat f1 < f2), insert D at gd and P at gp > gd on vehicle w:
+//       (L+1)(L+2)/2 candidates per entry, gd-major
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+template <typename OpT>
+__global__ void __launch_bounds__(256)
+ls_build_kernel(int kind, int n, int m, const int32_t *__restrict__ base_ops, const int32_t *__restrict__ base_lens,
+                const int32_t *__restrict__ entries, const int64_t *__restrict__ entry_start, int64_t n_entries,
+                const int64_t *__restrict__ index_list, int64_t first, int64_t count,
+                OpT *__restrict__ out_ops, int32_t *__restrict__ out_lens) {
+    const int lane = threadIdx.x & 31;
+    const int64_t cand = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (cand >= count) return;
+    const int64_t gidx = index_list ? index_list[cand] : first + cand;
+    const int n2 = 2 * n;
+    // ---- decode (all lanes redundantly; warp-uniform)
+    int64_t e;
+    if (kind == 0) {
+        e = gidx / (int64_t)(n2 + m - 2);
+    } else {
+        int64_t lo = 0, hi = n_entries - 1;  // last entry with start <= gidx
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (entry_start[mid] <= gidx) lo = mid; else hi = mid - 1;
+        }
+        e = lo;
+    }
+    const int32_t *E = entries + e * 5;
+    const int worker = E[0];
+    const int32_t *ops = base_ops + (int64_t)worker * n2;
+    const int32_t *lens = base_lens + (int64_t)worker * m;
+    int L_lane = lane < m ? lens[lane] : 0;
+    OpT *oo = out_ops + cand * n2;
+    int32_t *ol = out_lens + cand * m;
+    if (kind == 0) {
+        const int v = E[1], i = E[2], fi = E[3];
+        const int op = ops[fi];
+        int j = (int)(gidx - e * (int64_t)(n2 + m - 2));
+        // base lens, enumeration of (w, g) with (v, i) excluded
+        const int lb_lane = L_lane - (lane == v ? 1 : 0);
+        int ex = 0, w = 0, g = 0, boff = 0;
+        for (int u = 0; u < v; ++u) ex += __shfl_sync(VRP_FULL_MASK, lb_lane, u) + 1;
+        ex += i;
+        if (j >= ex) ++j;
+        for (int u = 0; u < m; ++u) {
+            const int gaps = __shfl_sync(VRP_FULL_MASK, lb_lane, u) + 1;
+            if (j < gaps) { w = u; g = j; break; }
+            j -= gaps;
+            boff += gaps - 1;
+        }
+        const int p = boff + g;
+        for (int o = lane; o < n2; o += 32) {
+            const int x = o < p ? o : o - 1;  // base index (unused when o == p)
+            const int val = o == p ? op : ops[x < fi ? x : x + 1];
+            oo[o] = (OpT)val;
+        }
+        if (lane < m) ol[lane] = lb_lane + (lane == w ? 1 : 0);
+    } else {
+        const int c = E[1], w = E[2], f1 = E[3], f2 = E[4];
+        const int64_t t = gidx - entry_start[e];
+        // stripped lens: c's ops removed from whichever routes hold them
+        int sl_lane = L_lane;
+        {
+            // route of flat position f: the lane whose [off, off+L) holds it
+            int off = L_lane;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(VRP_FULL_MASK, off, o);
+                if (lane >= o) off += y;
+            }
+            off -= L_lane;
+            if (lane < m) sl_lane -= (f1 >= off && f1 < off + L_lane) + (f2 >= off && f2 < off + L_lane);
+        }
+        int soff = 0;
+        for (int u = 0; u < w; ++u) soff += __shfl_sync(VRP_FULL_MASK, sl_lane, u);
+        const int Lw = __shfl_sync(VRP_FULL_MASK, sl_lane, w);
+        // t -> (gd, gp): S(gd) = gd (L+1) - gd (gd-1) / 2 pairs precede gd
+        const double A = 2.0 * Lw + 3.0;
+        int gd = (int)floor((A - sqrt(A * A - 8.0 * (double)t)) / 2.0);
+        if (gd < 0) gd = 0;
+        if (gd > Lw) gd = Lw;
+        auto S = [&](int64_t x) { return x * (Lw + 1) - x * (x - 1) / 2; };
+        while (gd > 0 && S(gd) > t) --gd;
+        while (gd < Lw && S(gd + 1) <= t) ++gd;
+        const int gp = gd + 1 + (int)(t - S(gd));
+        const int pd = soff + gd, pp = soff + gp;
+        const int dop = 2 * (c - 1), pop = dop + 1;
+        for (int o = lane; o < n2; o += 32) {
+            int val;
+            if (o == pd) val = dop;
+            else if (o == pp) val = pop;
+            else {
+                const int x = o < pd ? o : (o < pp ? o - 1 : o - 2);  // stripped index
+                val = ops[x + (x >= f1) + (x >= f2 - 1)];
+            }
+            oo[o] = (OpT)val;
+        }
+        if (lane < m) ol[lane] = sl_lane + (lane == w ? 2 : 0);
+    }
+}
+
+}  // namespace
+
+int launch_ls_build(int kind, int n, int m, const int32_t *base_ops, const int32_t *base_lens,
+                    const int32_t *entries, const int64_t *entry_start, int64_t n_entries,
+                    const int64_t *index_list, int64_t first, int64_t count, void *out_ops, int op_bytes,
+                    int32_t *out_lens, cudaStream_t stream) {
+    if (count <= 0) return 0;
+    const int wpb = 8;
+    const int64_t blocks = (count + wpb - 1) / wpb;
+    if (op_bytes == 2)
+        ls_build_kernel<int16_t><<<(unsigned)blocks, 32 * wpb, 0, stream>>>(
+            kind, n, m, base_ops, base_lens, entries, entry_start, n_entries, index_list, first, count,
+            (int16_t *)out_ops, out_lens);
+    else
+        ls_build_kernel<int32_t><<<(unsigned)blocks, 32 * wpb, 0, stream>>>(
+            kind, n, m, base_ops, base_lens, entries, entry_start, n_entries, index_list, first, count,
+            (int32_t *)out_ops, out_lens);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
