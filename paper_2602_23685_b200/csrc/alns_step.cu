@@ -566,7 +566,25 @@ __device__ void destroy(const DevInstance &I, int op, int q, int q_min, const in
     __syncwarp();
 }
 
+// Out-of-line copies of the once-per-iteration steps.  The warp-scan (SCAN)
+// instantiation calls these -- keeping its per-customer repair loop compact
+// in the instruction cache measured faster (kroA100/a280) -- while the
+// one-lane instantiation inlines them (faster at eil51's short routes).
 template <bool INTD>
+__device__ __noinline__ void destroy_ool(const DevInstance &I, int op, int q, int q_min, const int *cur,
+                                         const int *lens, Dx &D, int C, int lane, PhiloxGen &gen) {
+    destroy<INTD>(I, op, q, q_min, cur, lens, D, C, lane, gen);
+}
+__device__ __noinline__ void remove_flagged_ool(Ctx &X, const int *cur, const int *lens, Dx &D) {
+    remove_flagged(X, cur, lens, D);
+}
+template <bool INTD>
+__device__ __noinline__ int replay_ool(const DevInstance &I, const int *row, int L, int lane, Dx &D, double *z) {
+    return replay<INTD>(I, row, L, lane, D, false, false, z);
+}
+__device__ __noinline__ void store_rows_ool(const Ctx &X, int *ops, int *lens) { store_rows(X, ops, lens); }
+
+template <bool INTD, bool SCAN>
 __global__ void __launch_bounds__(32)
 alns_kernel(DevInstance I, vrp_alns_params P, vrp_alns_worker *__restrict__ workers, int32_t nw,
             int32_t *__restrict__ cur_ops, int32_t *__restrict__ cur_lens, int32_t *__restrict__ best_ops,
@@ -617,16 +635,24 @@ alns_kernel(DevInstance I, vrp_alns_params P, vrp_alns_worker *__restrict__ work
             __syncwarp();
         }
         // destroy + remove_customers (alns.py:574; insertion.py:379-397)
-        destroy<INTD>(I, dop, q, P.q_min, cur, clen, D, C, lane, gen);
-        remove_flagged(X, cur, clen, D);
+        if (SCAN) {
+            destroy_ool<INTD>(I, dop, q, P.q_min, cur, clen, D, C, lane, gen);
+            remove_flagged_ool(X, cur, clen, D);
+        } else {
+            destroy<INTD>(I, dop, q, P.q_min, cur, clen, D, C, lane, gen);
+            remove_flagged(X, cur, clen, D);
+        }
         // repair (alns.py:258-274): reinsert_all, then exact_makespan
-        rebuild_all(X);
+        rebuild_all<SCAN>(X);
         const int nrem = compact_flags(X, D.flag);
         const int rk = rop == 0 ? 0 : rop == 1 ? 2 : rop == 2 ? 3 : m;
-        int st = reinsert_core(X, nrem, rk, &gen, true);
+        int st = reinsert_core<SCAN>(X, nrem, rk, &gen, true);
         double zc = 0.0;
-        if (!st) st = replay<INTD>(I, X.seq + (size_t)(lane < m ? lane : 0) * C, lane < m ? X.Lr[lane] : 0,
-                                   lane, D, false, false, &zc);
+        if (!st) {
+            const int *row = X.seq + (size_t)(lane < m ? lane : 0) * C;
+            const int L = lane < m ? X.Lr[lane] : 0;
+            st = SCAN ? replay_ool<INTD>(I, row, L, lane, D, &zc) : replay<INTD>(I, row, L, lane, D, false, false, &zc);
+        }
         // acceptance + bookkeeping (alns.py:577-611)
         int acc = 0, nb = 0;
         if (lane == 0) {
@@ -688,8 +714,8 @@ alns_kernel(DevInstance I, vrp_alns_params P, vrp_alns_worker *__restrict__ work
         }
         acc = __shfl_sync(VRP_FULL_MASK, acc, 0);
         nb = __shfl_sync(VRP_FULL_MASK, nb, 0);
-        if (acc) store_rows(X, cur, clen);
-        if (nb) store_rows(X, best, blen);
+        if (acc) { if (SCAN) store_rows_ool(X, cur, clen); else store_rows(X, cur, clen); }
+        if (nb) { if (SCAN) store_rows_ool(X, best, blen); else store_rows(X, best, blen); }
         __syncwarp();
     }
     if (lane == 0) {
@@ -754,14 +780,12 @@ int launch_alns(const DevInstance &I, const vrp_alns_params &P, vrp_alns_worker 
     const size_t per = al8(alns_scratch_bytes(I.n, I.m));
     unsigned char *scratch = nullptr;
     if (cudaMallocAsync(&scratch, per * (size_t)nw, stream) != cudaSuccess) return -1;
-    if (I.integral)
-        alns_kernel<true><<<nw, 32, 0, stream>>>(I, P, workers, nw, cur_ops, cur_lens, best_ops, best_lens,
-                                                  q_draws, q_stride, it_begin, it_end, trace_it, trace_z,
-                                                  trace_cap, rows_it, rows_val, rows_cap, scratch, per);
-    else
-        alns_kernel<false><<<nw, 32, 0, stream>>>(I, P, workers, nw, cur_ops, cur_lens, best_ops, best_lens,
-                                                   q_draws, q_stride, it_begin, it_end, trace_it, trace_z,
-                                                   trace_cap, rows_it, rows_val, rows_cap, scratch, per);
+#define VRP_ALNS_ARGS I, P, workers, nw, cur_ops, cur_lens, best_ops, best_lens, q_draws, q_stride, it_begin, \
+        it_end, trace_it, trace_z, trace_cap, rows_it, rows_val, rows_cap, scratch, per
+    if (use_scan(I)) alns_kernel<true, true><<<nw, 32, 0, stream>>>(VRP_ALNS_ARGS);
+    else if (I.integral) alns_kernel<true, false><<<nw, 32, 0, stream>>>(VRP_ALNS_ARGS);
+    else alns_kernel<false, false><<<nw, 32, 0, stream>>>(VRP_ALNS_ARGS);
+#undef VRP_ALNS_ARGS
     const cudaError_t e = cudaPeekAtLastError();
     cudaFreeAsync(scratch, stream);
     return e == cudaSuccess ? 0 : -1;

@@ -31,6 +31,7 @@
 
 namespace {
 
+template <bool SCAN>
 __global__ void __launch_bounds__(128)
 repair_kernel(DevInstance I, const int32_t *__restrict__ pops, int64_t pstride,
               const int32_t *__restrict__ plens, const int32_t *__restrict__ removed, int64_t rstride,
@@ -74,7 +75,7 @@ repair_kernel(DevInstance I, const int32_t *__restrict__ pops, int64_t pstride,
     if (bad) {
         st = 2;  // malformed partial
     } else {
-        rebuild_all(X);
+        rebuild_all<SCAN>(X);
         // remaining = sorted(set(removed)) (insertion.py:488): mark, then compact
         for (int c = lane; c <= n; c += 32) X.s_has[c] = 0;
         __syncwarp();
@@ -85,7 +86,7 @@ repair_kernel(DevInstance I, const int32_t *__restrict__ pops, int64_t pstride,
         }
         __syncwarp();
         const int nrem = compact_flags(X, X.s_has);
-        st = reinsert_core(X, nrem, regret_k[inst], &gen, use_rng);
+        st = reinsert_core<SCAN>(X, nrem, regret_k[inst], &gen, use_rng);
     }
     // ---- write back
     int32_t *oo = out_ops + inst * ostride;
@@ -117,9 +118,14 @@ int launch_repair(const DevInstance &I, const int32_t *pops, int64_t pstride, co
     if (cudaMallocAsync(&scratch, per * (size_t)N, stream) != cudaSuccess) return -1;
     const int wpb = 4;
     const int64_t blocks = (N + wpb - 1) / wpb;
-    repair_kernel<<<(unsigned)blocks, 32 * wpb, 0, stream>>>(I, pops, pstride, plens, removed, rstride,
-                                                           nremoved, regret_k, states, out_ops, ostride,
-                                                           out_lens, status, scratch, N);
+    if (use_scan(I))
+        repair_kernel<true><<<(unsigned)blocks, 32 * wpb, 0, stream>>>(I, pops, pstride, plens, removed, rstride,
+                                                                     nremoved, regret_k, states, out_ops, ostride,
+                                                                     out_lens, status, scratch, N);
+    else
+        repair_kernel<false><<<(unsigned)blocks, 32 * wpb, 0, stream>>>(I, pops, pstride, plens, removed, rstride,
+                                                                      nremoved, regret_k, states, out_ops, ostride,
+                                                                      out_lens, status, scratch, N);
     const cudaError_t e = cudaPeekAtLastError();
     cudaFreeAsync(scratch, stream);
     return e == cudaSuccess ? 0 : -1;

@@ -128,12 +128,237 @@ struct Ctx {
     Opt *opts, *best;
     int *remaining;
     double *walk;
+    const double *dm, *pv;  // I->d, I->p
+    int pad_;
 
-    __device__ double d(int a, int b) const { return I->d[(int64_t)a * W + b]; }
-    __device__ double p(int c) const { return I->p[c]; }
+    __device__ double d(int a, int b) const { return dm[(int64_t)a * W + b]; }
+    __device__ double p(int c) const { return pv[c]; }
 };
 
 __device__ __forceinline__ int opc(int op) { return (op >> 1) + 1; }
+
+// ---------------------------------------------------------------------------
+// Warp-parallel passes for integral instances.  Every quantity the passes
+// form -- prefix sums of integer travel times, ready - T, T + runmax -- is an
+// exact integer below 2^53, so a tree-ordered scan gives the bit-identical
+// double the reference's left-to-right loop does; max/min/int scans are exact
+// for any data.  Non-integral instances keep the one-lane loops.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double scan_add(double x, int lane) {
+#pragma unroll 1
+    for (int o = 1; o < 32; o <<= 1) { const double y = __shfl_up_sync(VRP_FULL_MASK, x, o); if (lane >= o) x += y; }
+    return x;
+}
+__device__ __forceinline__ double scan_max(double x, int lane) {
+#pragma unroll 1
+    for (int o = 1; o < 32; o <<= 1) { const double y = __shfl_up_sync(VRP_FULL_MASK, x, o); if (lane >= o && y > x) x = y; }
+    return x;
+}
+__device__ __forceinline__ int scan_addi(int x, int lane) {
+#pragma unroll 1
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(VRP_FULL_MASK, x, o); if (lane >= o) x += y; }
+    return x;
+}
+__device__ __forceinline__ int scan_maxi(int x, int lane) {
+#pragma unroll 1
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(VRP_FULL_MASK, x, o); if (lane >= o && y > x) x = y; }
+    return x;
+}
+__device__ __forceinline__ int scan_mini(int x, int lane) {
+#pragma unroll 1
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_up_sync(VRP_FULL_MASK, x, o); if (lane >= o && y < x) x = y; }
+    return x;
+}
+__device__ __forceinline__ double rscan_max(double x, int lane) {
+#pragma unroll 1
+    for (int o = 1; o < 32; o <<= 1) { const double y = __shfl_down_sync(VRP_FULL_MASK, x, o); if (lane + o < 32 && y > x) x = y; }
+    return x;
+}
+__device__ __forceinline__ int rscan_addi(int x, int lane) {
+#pragma unroll 1
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_down_sync(VRP_FULL_MASK, x, o); if (lane + o < 32) x += y; }
+    return x;
+}
+__device__ __forceinline__ int rscan_maxi(int x, int lane) {
+#pragma unroll 1
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_down_sync(VRP_FULL_MASK, x, o); if (lane + o < 32 && y > x) x = y; }
+    return x;
+}
+__device__ __forceinline__ int rscan_mini(int x, int lane) {
+#pragma unroll 1
+    for (int o = 1; o < 32; o <<= 1) { const int y = __shfl_down_sync(VRP_FULL_MASK, x, o); if (lane + o < 32 && y < x) x = y; }
+    return x;
+}
+
+// pass1 (insertion.py:68-76), warp-wide
+__device__ void pass1_warp(Ctx &X, int v) {
+    const int L = X.Lr[v], lane = X.lane;
+    const int *sq = X.seq + (size_t)v * X.C;
+    double carry = 0.0;
+    int cprev = 0;
+    for (int base = 0; base < L; base += 32) {
+        const int i = base + lane;
+        const bool in = i < L;
+        const int op = in ? sq[i] : 0, c = opc(op);
+        int pc = __shfl_up_sync(VRP_FULL_MASK, c, 1);
+        if (lane == 0) pc = cprev;
+        const double t = carry + scan_add(in ? X.d(pc, c) : 0.0, lane);
+        if (in && !(op & 1)) {
+            X.ready[c] = t + X.p(c);
+            X.has_ready[c] = 1;
+            X.pos_v[c] = v;
+            X.pos_i[c] = i;
+        }
+        carry = __shfl_sync(VRP_FULL_MASK, t, 31);
+        cprev = __shfl_sync(VRP_FULL_MASK, c, 31);
+    }
+}
+
+// pass2 (insertion.py:78-144), warp-wide; the arrays' untouched defaults
+// (sp/lo_pre/hi_pre at 0, the suffix arrays at L) are the only init writes
+__device__ void pass2_warp(Ctx &X, int v) {
+    const int k = X.k, L = X.Lr[v], lane = X.lane;
+    const size_t o = (size_t)v * X.C, o1 = (size_t)v * (X.C + 1);
+    const int *sq = X.seq + o;
+    double *T = X.T + o, *dep = X.dep + o, *M = X.M + o;
+    int *sp = X.sp + o1, *lo_pre = X.lo_pre + o1, *hi_pre = X.hi_pre + o1;
+    int *lo_suf = X.lo_suf + o1, *hi_suf = X.hi_suf + o1, *drops = X.drops + o1;
+    if (lane == 0) {
+        sp[0] = 0; lo_pre[0] = 0; hi_pre[0] = k;
+        lo_suf[L] = NEG_BIG; hi_suf[L] = POS_BIG; drops[L] = 0;
+        if (!L) { X.ret[v] = 0.0; X.exit_leg[v] = 0.0; }
+    }
+    if (!L) { __syncwarp(); return; }
+    double ct = 0.0, crun = 0.0;
+    int cs = 0, clo = 0, chi = k, cprev = 0;
+    for (int base = 0; base < L; base += 32) {
+        const int i = base + lane;
+        const bool in = i < L;
+        const int op = in ? sq[i] : 0, c = opc(op);
+        const bool isp = in && (op & 1), isd = in && !(op & 1);
+        int pc = __shfl_up_sync(VRP_FULL_MASK, c, 1);
+        if (lane == 0) pc = cprev;
+        const double t = ct + scan_add(in ? X.d(pc, c) : 0.0, lane);
+        double run = scan_max(isp ? X.ready[c] - t : -INFINITY, lane);
+        if (crun > run) run = crun;
+        const int delta = isp ? 1 : (isd ? -1 : 0);
+        const int s_in = cs + scan_addi(delta, lane), s_bef = s_in - delta;
+        int lo = scan_maxi(isd ? 1 - s_bef : NEG_BIG, lane);
+        if (clo > lo) lo = clo;
+        int hi = scan_mini(isp ? k - 1 - s_bef : POS_BIG, lane);
+        if (chi < hi) hi = chi;
+        if (in) {
+            T[i] = t;
+            dep[i] = t + run;
+            sp[i + 1] = s_in;
+            lo_pre[i + 1] = lo;
+            hi_pre[i + 1] = hi;
+        }
+        ct = __shfl_sync(VRP_FULL_MASK, t, 31);
+        crun = __shfl_sync(VRP_FULL_MASK, run, 31);
+        cs = __shfl_sync(VRP_FULL_MASK, s_in, 31);
+        clo = __shfl_sync(VRP_FULL_MASK, lo, 31);
+        chi = __shfl_sync(VRP_FULL_MASK, hi, 31);
+        cprev = __shfl_sync(VRP_FULL_MASK, c, 31);
+    }
+    __syncwarp();
+    double csuf = -INFINITY;
+    int cslo = NEG_BIG, cshi = POS_BIG, cnd = 0;
+    for (int ch = (L - 1) >> 5; ch >= 0; --ch) {
+        const int i = (ch << 5) + lane;
+        const bool in = i < L;
+        const int op = in ? sq[i] : 0, c = opc(op);
+        const bool isp = in && (op & 1), isd = in && !(op & 1);
+        const int spi = in ? sp[i] : 0;
+        double mx = rscan_max(isp ? X.ready[c] - T[i] : -INFINITY, lane);
+        if (csuf > mx) mx = csuf;
+        int slo = rscan_maxi(isd ? 1 - spi : NEG_BIG, lane);
+        if (cslo > slo) slo = cslo;
+        int shi = rscan_mini(isp ? k - 1 - spi : POS_BIG, lane);
+        if (cshi < shi) shi = cshi;
+        const int nd = cnd + rscan_addi(isd ? 1 : 0, lane);
+        if (in) {
+            M[i] = mx;
+            lo_suf[i] = slo;
+            hi_suf[i] = shi;
+            drops[i] = nd;
+        }
+        csuf = __shfl_sync(VRP_FULL_MASK, mx, 0);
+        cslo = __shfl_sync(VRP_FULL_MASK, slo, 0);
+        cshi = __shfl_sync(VRP_FULL_MASK, shi, 0);
+        cnd = __shfl_sync(VRP_FULL_MASK, nd, 0);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        X.exit_leg[v] = X.d(opc(sq[L - 1]), 0);
+        X.ret[v] = dep[L - 1] + X.exit_leg[v];
+    }
+    __syncwarp();
+}
+
+// insert_op, warp-wide: shift [gap, L) up by one, chunks from the end
+__device__ void insert_op_warp(Ctx &X, int v, int gap, int op) {
+    int *sq = X.seq + (size_t)v * X.C;
+    const int L = X.Lr[v];
+    for (int hi = L; hi > gap; hi -= 32) {
+        const int i = hi - X.lane;
+        const bool in = i > gap;
+        const int val = in ? sq[i - 1] : 0;
+        __syncwarp();
+        if (in) sq[i] = val;
+        __syncwarp();
+    }
+    if (X.lane == 0) {
+        sq[gap] = op;
+        X.Lr[v] = L + 1;
+    }
+    __syncwarp();
+}
+
+// ret_after_drop (insertion.py:274-310), warp-wide: walk 1 is a prefix sum;
+// walk 2's t = max(t + d, r) unrolls to max(D_L, max_j (r_j - D_j) + D_L)
+__device__ double ret_after_drop_warp(const Ctx &X, int v, int gap, int c) {
+    const int L = X.Lr[v], lane = X.lane;
+    if (!L) return X.d(0, c) + X.d(c, 0);
+    const int *sq = X.seq + (size_t)v * X.C;
+    double *w = X.walk;
+    double carry = 0.0;
+    int cprev = 0;
+    for (int base = 0; base <= L; base += 32) {
+        const int j = base + lane;
+        const bool in = j <= L;
+        const int cc = in ? (j == gap ? c : opc(sq[j > gap ? j - 1 : j])) : 0;
+        int pc = __shfl_up_sync(VRP_FULL_MASK, cc, 1);
+        if (lane == 0) pc = cprev;
+        const double t = carry + scan_add(in ? X.d(pc, cc) : 0.0, lane);
+        if (in) w[j] = t;
+        carry = __shfl_sync(VRP_FULL_MASK, t, 31);
+        cprev = __shfl_sync(VRP_FULL_MASK, cc, 31);
+    }
+    __syncwarp();
+    double xm = -INFINITY;
+    for (int j = lane; j <= L; j += 32) {
+        if (j == gap) continue;
+        const int op = sq[j > gap ? j - 1 : j];
+        if (!(op & 1)) continue;
+        const int cc = opc(op);
+        double r;
+        if (X.pos_v[cc] == v) {
+            const int di = X.pos_i[cc] + (X.pos_i[cc] >= gap ? 1 : 0);
+            r = w[di] + X.p(cc);
+        } else {
+            r = X.has_ready[cc] ? X.ready[cc] : 0.0;
+        }
+        const double val = r - w[j];
+        if (val > xm) xm = val;
+    }
+    xm = warp_max(xm);
+    const double DL = w[L];
+    const int last = L == gap ? c : opc(sq[L - 1]);
+    const double t = xm > 0.0 ? DL + xm : DL;
+    __syncwarp();
+    return t + X.d(last, 0);
+}
 
 // insertion.py:68-76 (one lane)
 __device__ void pass1(Ctx &X, int v) {
@@ -239,14 +464,21 @@ __device__ void refresh(Ctx &X) {
     for (int v = 0; v < X.m; ++v) X.omax[v] = v == arg1 ? top2 : top1;
 }
 
+template <bool SCAN>
 __device__ void rebuild_all(Ctx &X) {
     for (int c = X.lane; c <= X.n; c += 32) {
         X.has_ready[c] = 0; X.pos_v[c] = -1; X.pos_i[c] = -1; X.ready[c] = 0.0;
     }
     __syncwarp();
-    for (int v = X.lane; v < X.m; v += 32) pass1(X, v);
-    __syncwarp();
-    for (int v = X.lane; v < X.m; v += 32) pass2(X, v);
+    if (SCAN) {
+        for (int v = 0; v < X.m; ++v) pass1_warp(X, v);
+        __syncwarp();
+        for (int v = 0; v < X.m; ++v) pass2_warp(X, v);
+    } else {
+        for (int v = X.lane; v < X.m; v += 32) pass1(X, v);
+        __syncwarp();
+        for (int v = X.lane; v < X.m; v += 32) pass2(X, v);
+    }
     __syncwarp();
     if (X.lane == 0) refresh(X);
     __syncwarp();
@@ -376,10 +608,10 @@ __device__ int pick_windowed(const Key *keys, int cnt, int lane, PhiloxGen *gen,
         if (j < seen + __popc(mk)) {
             const unsigned want = mk;
             // the (j - seen)-th set bit
-            int r = j - seen, pos = -1;
-            for (int b = 0; b < 32; ++b)
-                if ((want >> b) & 1u) { if (r == 0) { pos = b; break; } --r; }
-            return base + pos;
+            unsigned x = want;
+#pragma unroll 1
+            for (int r = j - seen; r > 0; --r) x &= x - 1;
+            return base + __ffs(x) - 1;
         }
         seen += __popc(mk);
     }
@@ -465,6 +697,7 @@ __device__ void swap_state(Ctx &X, int v) {
 }
 
 // insertion.py:429-472; options in X.opts, returns the count (warp-uniform)
+template <bool SCAN>
 __device__ int customer_options(Ctx &X, int c, PhiloxGen *gen, bool use_rng) {
     const int m = X.m, lane = X.lane;
     int nopt = 0;
@@ -482,7 +715,14 @@ __device__ int customer_options(Ctx &X, int c, PhiloxGen *gen, bool use_rng) {
         const int sel[3] = {s0, s1, s2};
         // re-score the shortlist exactly, one lane each; drop keys -> keys[cnt..cnt+3)
         Key dk = Key{0, 0, 0, 0, 0};
-        if (lane < ns) {
+        if (SCAN) {
+            for (int j = 0; j < ns; ++j) {
+                const int si = sel[j];
+                const int gd = X.keys[si].a, stl = X.keys[si].stale;
+                const double r = ret_after_drop_warp(X, vd, gd, c);
+                if (lane == j) dk = Key{cost_of(X, vd, r), stl, gd, 0, 0};
+            }
+        } else if (lane < ns) {
             const int si = sel[lane];
             const int g_drop = X.keys[si].a;
             const double r = ret_after_drop(X, vd, g_drop, c, X.walk + (size_t)lane * X.C);
@@ -496,7 +736,13 @@ __device__ int customer_options(Ctx &X, int c, PhiloxGen *gen, bool use_rng) {
         __syncwarp();
         // tentative_drop: save, insert D, rebuild route vd only
         swap_state<true>(X, vd);
-        if (lane == 0) {
+        if (SCAN) {
+            insert_op_warp(X, vd, g_drop, 2 * (c - 1));
+            pass1_warp(X, vd);
+            __syncwarp();
+            pass2_warp(X, vd);
+            if (lane == 0) refresh(X);
+        } else if (lane == 0) {
             insert_op(X, vd, g_drop, 2 * (c - 1));
             pass1(X, vd);
             pass2(X, vd);
@@ -547,6 +793,12 @@ __device__ int customer_options(Ctx &X, int c, PhiloxGen *gen, bool use_rng) {
 }
 
 
+// Warp-scan passes (SCAN = true) need an integral instance (every partial sum
+// an exact integer) and pay off once routes are long enough: 2n/m >= 24
+// (measured: eil51's ~17-op routes run faster with the one-lane loops, whose
+// compact code also suits the instruction cache when 8 warps share an SM).
+__host__ __device__ inline bool use_scan(const DevInstance &I) { return I.integral && 2 * I.n >= 24 * I.m; }
+
 // Bind a Ctx to one instance's scratch block `b` (make_layout(n, m) bytes).
 __device__ __forceinline__ void bind_ctx(Ctx &X, const DevInstance *I, unsigned char *b, int *Lr, int lane) {
     const Layout Ly = make_layout(I->n, I->m);
@@ -568,6 +820,7 @@ __device__ __forceinline__ void bind_ctx(Ctx &X, const DevInstance *I, unsigned 
     X.gl_g = (int *)(b + Ly.gl_g); X.gl_ret = (double *)(b + Ly.gl_ret); X.gl_stale = (int *)(b + Ly.gl_stale);
     X.keys = (Key *)(b + Ly.keys); X.opts = (Opt *)(b + Ly.opts); X.best = (Opt *)(b + Ly.best);
     X.remaining = (int *)(b + Ly.remaining); X.walk = (double *)(b + Ly.walk);
+    X.dm = I->d; X.pv = I->p;
 }
 
 // remaining = sorted customers c with flag[c] != 0 (insertion.py:488); returns the count
@@ -587,6 +840,7 @@ __device__ __forceinline__ int compact_flags(Ctx &X, const int *flag) {
 
 // insertion.py:484-516 on the context's current routes (already rebuilt) and
 // X.remaining[0..nrem).  Returns 0, or 1 for RepairFailed.
+template <bool SCAN>
 __device__ int reinsert_core(Ctx &X, int nrem, int rk, PhiloxGen *gen, bool use_rng) {
     const int lane = X.lane;
     int st = 0;
@@ -595,7 +849,7 @@ __device__ int reinsert_core(Ctx &X, int nrem, int rk, PhiloxGen *gen, bool use_
         if (rk == 0) {
             for (int i = 0; i < nrem; ++i) {
                 const int c = X.remaining[i];
-                const int no = customer_options(X, c, gen, use_rng);
+                const int no = customer_options<SCAN>(X, c, gen, use_rng);
                 if (!no) { st = 1; break; }
                 if (lane == 0) X.best[i] = X.opts[0];
                 __syncwarp();
@@ -612,7 +866,7 @@ __device__ int reinsert_core(Ctx &X, int nrem, int rk, PhiloxGen *gen, bool use_
             bool have = false;
             for (int i = 0; i < nrem; ++i) {
                 const int c = X.remaining[i];
-                const int no = customer_options(X, c, gen, use_rng);
+                const int no = customer_options<SCAN>(X, c, gen, use_rng);
                 if (!no) { st = 1; break; }
                 if (lane == 0) {
                     double regret;
@@ -644,16 +898,29 @@ __device__ int reinsert_core(Ctx &X, int nrem, int rk, PhiloxGen *gen, bool use_
         const Opt o = rk == 0 ? X.best[chosen] : X.best[0];
         const int c = X.remaining[chosen];
         if (o.pair) {
-            if (lane == 0) { insert_op(X, o.vd, o.gd, 2 * (c - 1) + 1); insert_op(X, o.vd, o.gd, 2 * (c - 1)); }
-            __syncwarp();
-            rebuild_all(X);
+            if (SCAN) {
+                insert_op_warp(X, o.vd, o.gd, 2 * (c - 1) + 1);
+                insert_op_warp(X, o.vd, o.gd, 2 * (c - 1));
+            } else {
+                if (lane == 0) { insert_op(X, o.vd, o.gd, 2 * (c - 1) + 1); insert_op(X, o.vd, o.gd, 2 * (c - 1)); }
+                __syncwarp();
+            }
+            rebuild_all<SCAN>(X);
         } else {
-            if (lane == 0) insert_op(X, o.vd, o.gd, 2 * (c - 1));
-            __syncwarp();
-            rebuild_all(X);
-            if (lane == 0) insert_op(X, o.vp, o.gp, 2 * (c - 1) + 1);
-            __syncwarp();
-            rebuild_all(X);
+            if (SCAN) {
+                insert_op_warp(X, o.vd, o.gd, 2 * (c - 1));
+            } else {
+                if (lane == 0) insert_op(X, o.vd, o.gd, 2 * (c - 1));
+                __syncwarp();
+            }
+            rebuild_all<SCAN>(X);
+            if (SCAN) {
+                insert_op_warp(X, o.vp, o.gp, 2 * (c - 1) + 1);
+            } else {
+                if (lane == 0) insert_op(X, o.vp, o.gp, 2 * (c - 1) + 1);
+                __syncwarp();
+            }
+            rebuild_all<SCAN>(X);
         }
         if (lane == 0)
             for (int i = chosen; i + 1 < nrem; ++i) X.remaining[i] = X.remaining[i + 1];

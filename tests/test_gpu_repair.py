@@ -86,3 +86,37 @@ def test_reinsert_all_api_toy():  # test_alns.py:107-116: the toy rebuilds to 47
     ctx = INS.InsertionContext(toy, [[]])
     INS.reinsert_all(ctx, [1, 2], 0, np.random.Generator(np.random.Philox(key=(1, 1))))
     assert evaluate(toy, ctx.solution()).makespan == 47
+
+
+def test_repair_non_integral_instance_vs_oracle():
+    """fp64 instance (no exact-integer sums): K5 keeps the reference's
+    left-to-right passes; integral instances take the warp-scan passes."""
+    from paper_2602_23685_b200.instance import Instance
+    base = config_instance("kroA100")
+    d, p = base.arrays()
+    rng = np.random.default_rng(11)
+    d2 = d + rng.random(d.shape) * 0.61
+    d2 = (d2 + d2.T) / 2
+    np.fill_diagonal(d2, 0.0)
+    p2 = p * 1.0003 + rng.random(p.shape) / 7
+    p2[0] = 0.0
+    inst = Instance.from_arrays(d2, p2, base.m, base.k, label="kro-frac")
+    count = 24
+    dec = O.decode_batch(inst, I.chromosomes(inst.n, count, (64, 3)))
+    parts, plens, removed, rks = [], [], [], []
+    for i in range(count):
+        pick = I.philox(65, 3, i).choice(np.arange(1, inst.n + 1), size=9, replace=False)
+        o, l, r = O.remove_customers(inst, dec["ops"][i], dec["lens"][i], pick)
+        parts.append(o[:2 * inst.n]); plens.append(l); removed.append(r)
+        rks.append((0, 2, 3, inst.m)[i % 4])
+    parts, plens = np.stack(parts), np.stack(plens)
+    dev_gens = [I.philox(66, 3, i) for i in range(count)]
+    o, l, st = INS.reinsert_batch(inst, parts, plens, removed, rks, dev_gens)
+    for i in range(count):
+        g = I.philox(66, 3, i)
+        rst, ro, rl = O.reinsert_all(inst, parts[i], plens[i], removed[i], rks[i], g)
+        assert st[i] == rst, i
+        if rst == 0:
+            np.testing.assert_array_equal(l[i], rl)
+            np.testing.assert_array_equal(o[i], ro)
+        assert same_state(dev_gens[i], g), i
