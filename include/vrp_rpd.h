@@ -160,7 +160,8 @@ int vrp_destroy_batch(vrp_instance_t h, const int32_t *ops, int64_t op_stride, c
                       int64_t removed_stride, int32_t *nremoved, int64_t N, void *stream);
 
 /* Local-search neighbourhoods (alns.py:416-487 pickup_repositioning /
- * cross_agent_relocation) materialised as a candidate batch for
+ * cross_agent_relocation; baselines.py:372-455 two_opt_improve) materialised
+ * as a candidate batch for
  * vrp_makespan_batch (K2 estimate, K1 verify).  Candidates are numbered in the
  * reference's generation order:
  *   kind 0 (pickup move): entries[e] = {worker, v, i, fi, 0} -- the pickup at
@@ -170,6 +171,11 @@ int vrp_destroy_batch(vrp_instance_t h, const int32_t *ops, int64_t op_stride, c
  *   kind 1 (cross move): entries[e] = {worker, c, w, f1, f2} -- customer c
  *     (flat op positions f1 < f2) is stripped and re-inserted as D at gd, P at
  *     gp (0 <= gd < gp <= L_w + 1) on vehicle w: entry_start[e] = first index
+ *   kind 2 (2-opt, baselines.py:393-406): entries[e] = {worker, v, 0, 0, 0} --
+ *     reverse positions i < j of route v, L_v (L_v - 1) / 2 candidates, i-major
+ *   kind 3 (swap, baselines.py:431-443): entries[e] = {worker, 0, 0, 0, 0} --
+ *     swap flat ops a < b, 2n (2n - 1) / 2 candidates, a-major
+ *   (two_opt_improve's relocation, :408-429, is kind 0 over every op)
  *   base_ops[W][2n], base_lens[W][m]: the workers' solutions (DEVICE)
  *   index_list (nullable): explicit candidate indices; else first .. first+count-1
  *   out_ops[count][2n] (op_bytes 2 or 4), out_lens[count][m] */

@@ -1,0 +1,93 @@
+"""Heuristic polish on the device -- drop-in for the reference's
+``baselines.two_opt_improve`` (``/root/reference/pkg/src/vrp_rpd/baselines.py:372-455``,
+SURVEY §8(f) row 3).
+
+The reference scans three neighbourhoods in a fixed order -- intra-route
+2-opt reversal, single-operation relocation, pairwise swap -- re-scoring every
+candidate with ``evaluate`` and taking the FIRST strict improvement
+(< best - 1e-9), restarting from 2-opt after each one, until a fixed point or
+the move budget (default 50n evaluated candidates) runs out.
+
+Here each scan is evaluated chunk by chunk: ``vrp_ls_build`` materialises the
+next candidates of the current neighbourhood in the reference's order
+(kinds 2 / 0 / 3), K1 scores them with ``evaluate`` semantics, and the first
+improving index in the chunk is exactly the reference's next accepted move
+(everything before it was non-improving).  The budget is charged as the
+reference charges it: the candidates up to and including the accepted one,
+or the whole chunk when none improves; chunks never exceed the remaining
+budget.  Candidates evaluated past the accepted one are speculation the
+reference never sees, so the result is bit-identical."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import device as DV
+from .localsearch import _build
+from .schedule import Solution, evaluate
+
+CHUNK = 1 << 15
+
+
+def _phase_entries(kind, lens, n):
+    """Entries + candidate counts of one neighbourhood (zero-count entries
+    dropped so that entry_start stays strictly increasing)."""
+    m = lens.size
+    if kind == 2:  # 2-opt: routes in order
+        ent = [(0, v, 0, 0, 0) for v in range(m) if lens[v] >= 2]
+        cnt = [int(lens[v]) * (int(lens[v]) - 1) // 2 for v in range(m) if lens[v] >= 2]
+    elif kind == 0:  # relocation: every op in route order
+        off = np.concatenate([[0], np.cumsum(lens)[:-1]])
+        ent = [(0, v, i, int(off[v] + i), 0) for v in range(m) for i in range(int(lens[v]))]
+        cnt = [2 * n + m - 2] * len(ent)
+    else:  # swap: one entry, all flat pairs
+        ent = [(0, 0, 0, 0, 0)]
+        cnt = [2 * n * (2 * n - 1) // 2]
+    return np.asarray(ent, np.int32).reshape(-1, 5), np.asarray(cnt, np.int64)
+
+
+def two_opt_improve(instance, solution: Solution, move_budget: int | None = None,
+                    chunk: int = CHUNK) -> Solution:
+    """First-improvement 2-opt / relocate / swap polish (baselines.py:372-455)."""
+    n = instance.n
+    budget = move_budget if move_budget is not None else 50 * n
+    dev = torch.device("cuda", torch.cuda.current_device())
+    o, l = solution.to_arrays(n)
+    ops_t = torch.from_numpy(np.ascontiguousarray(o[None, :2 * n])).to(dev)
+    lens_t = torch.from_numpy(np.ascontiguousarray(l[None])).to(dev)
+    best = evaluate(instance, solution).makespan
+    improved = True
+    while improved and budget > 0:
+        improved = False
+        lens = lens_t[0].cpu().numpy()
+        for kind in (2, 0, 3):
+            ent, cnt = _phase_entries(kind, lens, n)
+            total = int(cnt.sum())
+            if total == 0:
+                continue
+            starts = np.zeros(len(cnt), np.int64)
+            np.cumsum(cnt[:-1], out=starts[1:])
+            ent_t = torch.from_numpy(ent).to(dev)
+            start_t = torch.from_numpy(starts).to(dev)
+            pos = 0
+            while pos < total and budget > 0:
+                k = min(chunk, total - pos, budget)
+                c_ops, c_lens = _build(instance, kind, ops_t, lens_t, ent_t, start_t, pos, k,
+                                       op_dtype=torch.int32)
+                r = DV.makespan_batch(instance, c_ops, c_lens, mode=N.MODE_EVALUATE)
+                ok = (r["status"] == 0) & (r["z"] < best - 1e-9)
+                hit = torch.nonzero(ok)
+                if hit.numel():
+                    j = int(hit[0, 0])
+                    budget -= j + 1
+                    best = float(r["z"][j])
+                    ops_t = c_ops[j:j + 1].clone()
+                    lens_t = c_lens[j:j + 1].clone()
+                    improved = True
+                    break
+                budget -= k
+                pos += k
+            if improved or budget <= 0:
+                break
+    return Solution.from_arrays(ops_t[0].cpu().numpy(), lens_t[0].cpu().numpy())

@@ -262,11 +262,11 @@ int vrp_ls_build(vrp_instance_t h, int32_t kind, const int32_t *base_ops, const 
                  const int64_t *index_list, int64_t first, int64_t count, void *out_ops,
                  int32_t op_bytes, int32_t *out_lens, void *stream) {
     if (!h) return fail(VRP_EINVAL, "null instance%s");
-    if (kind != 0 && kind != 1) return fail(VRP_EINVAL, "vrp_ls_build: kind must be 0 or 1%s");
+    if (kind < 0 || kind > 3) return fail(VRP_EINVAL, "vrp_ls_build: kind must lie in 0..3%s");
     if (op_bytes != 2 && op_bytes != 4) return fail(VRP_EINVAL, "vrp_ls_build: op_bytes must be 2 or 4%s");
     if (count < 0 || n_entries < 0) return fail(VRP_EINVAL, "vrp_ls_build: negative count%s");
     if (count == 0) return 0;
-    if (!base_ops || !base_lens || !entries || !out_ops || !out_lens || (kind == 1 && !entry_start) ||
+    if (!base_ops || !base_lens || !entries || !out_ops || !out_lens || (kind != 0 && !entry_start) ||
         n_entries == 0)
         return fail(VRP_EINVAL, "vrp_ls_build: null buffer%s");
     if (op_bytes == 2 && 2 * (int64_t)h->dev.n > 32767)

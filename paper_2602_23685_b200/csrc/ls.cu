@@ -13,12 +13,30 @@
 //   cross move   (entry = worker, c, w, f1, f2): strip customer c's two ops
 //       (flat f1 < f2), insert D at gd and P at gp > gd on vehicle w:
 //       (L+1)(L+2)/2 candidates per entry, gd-major
+// and the two_opt_improve neighbourhoods (baselines.py:372-455):
+//   2-opt        (entry = worker, v): reverse positions i < j of route v,
+//       L(L-1)/2 candidates, i-major
+//   swap         (entry = worker): swap flat ops a < b, 2n(2n-1)/2, a-major
+// (its relocation neighbourhood is the pickup move applied to every op)
 #include <math.h>
 
 #include "common.cuh"
 #include "kernels.h"
 
 namespace {
+
+// t-th pair (x, y), 0 <= x < y < K, in x-major order: S(x) = x (K-1) - x (x-1) / 2
+__device__ __forceinline__ void tri_decode(int64_t t, int K, int &x, int &y) {
+    const double A = 2.0 * K - 1.0;
+    int g = (int)floor((A - sqrt(A * A - 8.0 * (double)t)) / 2.0);
+    if (g < 0) g = 0;
+    if (g > K - 2) g = K - 2;
+    auto S = [&](int64_t q) { return q * (K - 1) - q * (q - 1) / 2; };
+    while (g > 0 && S(g) > t) --g;
+    while (g < K - 2 && S(g + 1) <= t) ++g;
+    x = g;
+    y = g + 1 + (int)(t - S(g));
+}
 
 template <typename OpT>
 __global__ void __launch_bounds__(256)
@@ -73,6 +91,25 @@ ls_build_kernel(int kind, int n, int m, const int32_t *__restrict__ base_ops, co
             oo[o] = (OpT)val;
         }
         if (lane < m) ol[lane] = lb_lane + (lane == w ? 1 : 0);
+    } else if (kind == 2 || kind == 3) {
+        // kind 2: reverse positions i..j of route E[1]; kind 3: swap flat ops a < b
+        const int64_t t = gidx - entry_start[e];
+        int lo, hi;
+        if (kind == 2) {
+            const int v = E[1];
+            int off = 0;
+            for (int u = 0; u < v; ++u) off += __shfl_sync(VRP_FULL_MASK, L_lane, u);
+            const int Lv = __shfl_sync(VRP_FULL_MASK, L_lane, v);
+            int i, j;
+            tri_decode(t, Lv, i, j);
+            lo = off + i;
+            hi = off + j;
+            for (int o = lane; o < n2; o += 32) oo[o] = (OpT)ops[(o >= lo && o <= hi) ? lo + hi - o : o];
+        } else {
+            tri_decode(t, n2, lo, hi);
+            for (int o = lane; o < n2; o += 32) oo[o] = (OpT)ops[o == lo ? hi : (o == hi ? lo : o)];
+        }
+        if (lane < m) ol[lane] = L_lane;
     } else {
         const int c = E[1], w = E[2], f1 = E[3], f2 = E[4];
         const int64_t t = gidx - entry_start[e];
@@ -92,15 +129,8 @@ ls_build_kernel(int kind, int n, int m, const int32_t *__restrict__ base_ops, co
         int soff = 0;
         for (int u = 0; u < w; ++u) soff += __shfl_sync(VRP_FULL_MASK, sl_lane, u);
         const int Lw = __shfl_sync(VRP_FULL_MASK, sl_lane, w);
-        // t -> (gd, gp): S(gd) = gd (L+1) - gd (gd-1) / 2 pairs precede gd
-        const double A = 2.0 * Lw + 3.0;
-        int gd = (int)floor((A - sqrt(A * A - 8.0 * (double)t)) / 2.0);
-        if (gd < 0) gd = 0;
-        if (gd > Lw) gd = Lw;
-        auto S = [&](int64_t x) { return x * (Lw + 1) - x * (x - 1) / 2; };
-        while (gd > 0 && S(gd) > t) --gd;
-        while (gd < Lw && S(gd + 1) <= t) ++gd;
-        const int gp = gd + 1 + (int)(t - S(gd));
+        int gd, gp;  // D at gd, P at gp: pairs of [0, Lw + 1]
+        tri_decode(t, Lw + 2, gd, gp);
         const int pd = soff + gd, pp = soff + gp;
         const int dop = 2 * (c - 1), pop = dop + 1;
         for (int o = lane; o < n2; o += 32) {

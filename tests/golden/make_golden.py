@@ -364,6 +364,20 @@ def main():
         np.random.PCG64 = orig_pcg
     meta["pipelines"] = pipes
 
+    # ---- heuristic polish two_opt_improve (baselines.py:372-455), deterministic
+    from vrp_rpd import baselines as R_base
+    polish = []
+    for key, cases, budget in (("gr17", 3, None), ("eil51", 2, 1500), ("kroA100", 1, 400)):
+        inst = insts.get(key) or ref_instance(key)
+        for j in range(cases):
+            sol = to_solution(blob[f"{key}/dec_ops"][j], blob[f"{key}/dec_lens"][j])
+            out = R_base.two_opt_improve(inst, sol, move_budget=budget)
+            o, l = I.lists_to_arrays([[(c, kd.value) for c, kd in t] for t in out.tours], inst.n)
+            blob[f"polish/{len(polish)}/ops"], blob[f"polish/{len(polish)}/lens"] = o, l
+            polish.append({"key": key, "case": j, "budget": budget})
+    meta["polish"] = polish
+    print(f"two_opt done at {time.time() - t0:.1f}s", flush=True)
+
     # ---- hint vehicle edge cases (brkga.py:82-89)
     genes = np.array([0.0, 1 / 3, 2 / 3, 1 / 6, 0.5, np.nextafter(1.0, 0), 0.999999999,
                       np.nextafter(1 / 3, 0), np.nextafter(2 / 3, 0), 0.2, 0.4, 0.6, 0.8])
