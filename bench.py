@@ -140,7 +140,7 @@ def make_candidates(inst, count: int, seed: int, device, chunk: int = 1 << 16):
     return ops, lens, z
 
 
-def extra_rates(device, ops, lens, decode_ms, n_dec):
+def extra_rates(device, ops, lens, decode_ms, n_dec, pipeline_seconds=30.0):
     """Secondary §8 throughputs on this GPU (not the headline): K3 decodes/s
     (the bench set-up, CUDA-event timed), BRKGA generations/s at paper scale
     (N_p = 30,000) on the a280 island config and dsj1000, ALNS repairs/s
@@ -194,6 +194,14 @@ def extra_rates(device, ops, lens, decode_ms, n_dec):
     dw.run(6, 100)
     torch.cuda.synchronize()
     out["alns_iterations_per_s_eil51_1184_workers"] = 1184 * 95 / (time.perf_counter() - t0)
+    if pipeline_seconds > 0:
+        # BASELINE's "best makespan at fixed time": the whole ALNS -> BRKGA
+        # pipeline (pipeline.run_pipeline_budget) on the kroA100 pipeline config
+        from paper_2602_23685_b200.pipeline import run_pipeline_budget
+        kro = config_instance("kroA100")
+        _, zb, tr = run_pipeline_budget(kro, seconds=pipeline_seconds)
+        out[f"best_makespan_kroA100_{pipeline_seconds:g}s"] = zb
+        out[f"initial_makespan_kroA100"] = tr[0][1]
     return {k: round(v, 2) for k, v in out.items()}
 
 
@@ -363,7 +371,7 @@ def run_gpu(args):
                 "gpu_launches": args.steps, "clocks": clk.summary(),
                 "setup_s": round(setup_s, 2)}
         if not args.no_extra and world == 1:
-            line["extra"] = extra_rates(dev, ops, lens, decode_ms, n_cand)
+            line["extra"] = extra_rates(dev, ops, lens, decode_ms, n_cand, args.pipeline_seconds)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -382,6 +390,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--pipeline-seconds", type=float, default=30.0,
+                    help="wall-clock budget of the best-makespan pipeline extra (0 = skip)")
     ap.add_argument("--no-verify", action="store_true", help="skip the K1 == decoder check (ablation builds)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -20,6 +20,7 @@ generator.
 from __future__ import annotations
 
 import math
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -356,9 +357,11 @@ def warm_start_population(instance, alns_solution: Solution, params: BrkgaParams
 # --------------------------------------------------------------------------
 
 def run_brkga(instance, params: BrkgaParams, warm_population=None, seed: int = 0, rng=None,
-              stream=None):
+              stream=None, deadline: float | None = None):
     """Evolve for params.generations generations entirely on the GPU; returns
-    (best Solution, BrkgaStats) like brkga.py:432-471."""
+    (best Solution, BrkgaStats) like brkga.py:432-471.  ``deadline``
+    (time.perf_counter() value, not in the reference) stops early at a
+    generation boundary -- the time-budgeted pipeline uses it."""
     gen = R.as_philox(rng) if rng is not None else R.philox_generator(seed, R.BRKGA_STREAM)
     if warm_population is not None:
         host = np.array(warm_population, dtype=float, copy=True)
@@ -394,7 +397,13 @@ def run_brkga(instance, params: BrkgaParams, warm_population=None, seed: int = 0
 
     decode_rows(pop, fits)
     best_update(fits, 0, pop, 0)
+    done = params.generations
     for g in range(1, params.generations + 1):
+        if deadline is not None and g % 2 == 1:
+            torch.cuda.synchronize()
+            if time.perf_counter() >= deadline:
+                done = g - 1
+                break
         evolve_device(pop, fits, params, state, out=pop2, order=order, elite_fit=elite_fit,
                       stream=stream)
         fits2[:n_elite].copy_(elite_fit[:n_elite])
@@ -406,8 +415,8 @@ def run_brkga(instance, params: BrkgaParams, warm_population=None, seed: int = 0
         fits, fits2 = fits2, fits
     R.state_from_device(gen, state)
     best = _result(decode_population(instance, best_genes.view(1, G), params, stream=stream), 0)
-    tr = trace.cpu().tolist()
-    stats = BrkgaStats(generations=params.generations,
-                       decodes=size + params.generations * (size - n_elite),
+    tr = trace.cpu().tolist()[:done + 1]
+    stats = BrkgaStats(generations=done,
+                       decodes=size + done * (size - n_elite),
                        best_fitness=best.fitness, trace=list(enumerate(tr)))
     return best.solution, stats

@@ -32,46 +32,72 @@ def run_pipeline(instance, alns_params: A.AlnsParams, brkga_params: B.BrkgaParam
     return (refined if z_ref <= z_inc else incumbent), incumbent
 
 
-def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.5, pool_size: int = 32,
+def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_size: int = 296,
                         alns_params: A.AlnsParams | None = None,
                         brkga_params: B.BrkgaParams | None = None, seed: int = 0,
-                        initial: Solution | None = None):
+                        initial: Solution | None = None, fit_cooling: bool = True):
     """Best makespan found within a wall-clock budget (the BASELINE metric's
-    'best makespan at fixed time'): device-resident ALNS workers (one warp
-    each, vrp_alns_iterate) for ``alns_share`` of the budget, then BRKGA generations
-    warm-started from the ALNS incumbent for the rest.  Returns
-    (best Solution, best makespan, trace [(seconds, best)])."""
+    'best makespan at fixed time'; the reference has no budget).
+
+    Stage 1, ``alns_share`` of the budget: ``pool_size`` device-resident ALNS
+    workers (one warp each, vrp_alns_iterate) in pools of
+    ``workers_per_pool`` that poll their pool's incumbent.  With
+    ``fit_cooling`` the SA schedule is fitted to the budget: a 10-iteration
+    calibration stretch measures the iteration rate, and the cooling rate is
+    set so that the temperature falls to 1e-3 of its start by the end of the
+    stage (the reference's alpha = 0.9998 assumes 20,000 iterations).
+    Stage 2, the rest: one BRKGA run (device generation loop) warm-started
+    from the ALNS incumbent, stopped at the deadline.
+    Returns (best Solution, best makespan, trace [(seconds, best)])."""
     t0 = time.perf_counter()
-    alns_params = alns_params or A.AlnsParams(max_iter=200_000)
-    brkga_params = brkga_params or B.BrkgaParams(population=4096, generations=1)
+    brkga_params = brkga_params or B.BrkgaParams(population=8192, generations=10**6)
     trace = []
     init = initial if initial is not None else A.construct_initial(instance, seed)
-    workers = [A._Worker(instance, alns_params, A.worker_seed(seed, i), init, None, None, i)
-               for i in range(pool_size)]
-    best = min(((w.z_best, w.best) for w in workers), key=lambda x: x[0])
-    trace.append((time.perf_counter() - t0, best[0]))
+    z0 = evaluate(instance, init).makespan
+    best = (z0, init)
+    trace.append((time.perf_counter() - t0, z0))
+    alns_end = t0 + alns_share * seconds
+    if alns_params is None:
+        alns_params = A.AlnsParams(max_iter=10)
+        if fit_cooling:  # calibration stretch: iteration time of this pool on this instance
+            probe = [A._Worker(instance, alns_params, A.worker_seed(seed + 1, i), init, None, None, i)
+                     for i in range(pool_size)]
+            t1 = time.perf_counter()
+            A._DeviceWorkers(instance, alns_params, probe).run(1, 10)
+            per_iter = (time.perf_counter() - t1) / 10
+            iters = max(50, int((alns_end - time.perf_counter()) / per_iter))
+            check = max(25, iters // 20)
+            alns_params = A.AlnsParams(max_iter=int(iters * 1.5) + 100,
+                                       alpha=min(0.99999, max(0.9, 1e-3 ** (1.0 / iters))),
+                                       best_check_interval=check, pool_sync_interval=check)
+        else:
+            alns_params = A.AlnsParams(max_iter=200_000)
+    if alns_params.max_iter and time.perf_counter() < alns_end:
+        wpp = alns_params.workers_per_pool
+        n_pools = (pool_size + wpp - 1) // wpp
+        pools = [A._PoolShare() for _ in range(n_pools)]
+        gshare = A._PoolShare() if n_pools > 1 else None
+        workers = [A._Worker(instance, alns_params, A.worker_seed(seed, i), init,
+                             pools[i // wpp] if pool_size > 1 else None, gshare if pool_size > 1 else None, i)
+                   for i in range(pool_size)]
 
-    def stop():
-        nonlocal best
-        w = min(workers, key=lambda w: w.z_best)
-        if w.z_best < best[0]:
-            best = (w.z_best, w.best)
-            trace.append((time.perf_counter() - t0, best[0]))
-        return time.perf_counter() - t0 >= alns_share * seconds
+        def stop():
+            nonlocal best
+            w = min(workers, key=lambda w: w.z_best)
+            if w.z_best < best[0]:
+                best = (w.z_best, w.best)
+                trace.append((time.perf_counter() - t0, best[0]))
+            return time.perf_counter() >= alns_end
 
-    if alns_params.max_iter:
         A._DeviceWorkers(instance, alns_params, workers).drive(stop=stop, max_stretch=25)
     incumbent = best[1]
-    rng = R.philox_generator(A.worker_seed(seed, 7001), R.BRKGA_STREAM)
-    pop = B.warm_start_population(instance, incumbent, brkga_params, rng)
-    gen = 0
-    while time.perf_counter() - t0 < seconds:
-        gen += 1
-        sol, stats = B.run_brkga(instance, brkga_params, warm_population=pop,
-                                 seed=A.worker_seed(seed, 7002 + gen))
+    if time.perf_counter() < t0 + seconds:
+        rng = R.philox_generator(A.worker_seed(seed, 7001), R.BRKGA_STREAM)
+        pop = B.warm_start_population(instance, incumbent, brkga_params, rng)
+        sol, _ = B.run_brkga(instance, brkga_params, warm_population=pop, seed=A.worker_seed(seed, 7002),
+                             deadline=t0 + seconds)
         z = evaluate(instance, sol).makespan
         if z < best[0]:
             best = (z, sol)
             trace.append((time.perf_counter() - t0, z))
-        pop = B.warm_start_population(instance, best[1], brkga_params, rng)
     return best[1], best[0], trace
