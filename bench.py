@@ -154,16 +154,19 @@ def extra_rates(device, ops, lens, decode_ms, n_dec, pipeline_seconds=30.0):
     from paper_2602_23685_b200.configs import config_instance
     out = {"decodes_per_s_dsj1000_random": n_dec / (decode_ms / 1e3)}
     for key in ("a280", "dsj1000"):
+        # generations/s of the device loop: (10 - 2) generations over the
+        # difference of two runs, so the population set-up cancels out
         inst = config_instance(key)
-        params = B.BrkgaParams(population=30000, generations=1)
-        B.run_brkga(inst, params, seed=0)  # warm
-        params = B.BrkgaParams(population=30000, generations=4)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        _, st = B.run_brkga(inst, params, seed=1)
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        out[f"brkga_generations_per_s_{key}_Np30000"] = 4 / el
+        B.run_brkga(inst, B.BrkgaParams(population=30000, generations=1), seed=0)  # warm
+        el = {}
+        for T in (2, 10):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            B.run_brkga(inst, B.BrkgaParams(population=30000, generations=T), seed=1)
+            torch.cuda.synchronize()
+            el[T] = time.perf_counter() - t0
+        out[f"brkga_generations_per_s_{key}_Np30000"] = 8 / (el[10] - el[2])
+        out[f"brkga_setup_plus_2_generations_s_{key}"] = el[2]
     inst = config_instance("eil51")
     cnt = 1024
     genes = I.chromosomes(inst.n, cnt, (7, 7))

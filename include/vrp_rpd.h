@@ -129,6 +129,12 @@ int vrp_best_update(const double *fitness, int64_t lo, int64_t hi, const double 
                     int64_t genes_per_row, double *best_fitness, double *best_genes,
                     int64_t *best_index, double *trace_slot, void *stream);
 
+/* Generator.random(count) on the device: out[i] = the i-th (next64 >> 11) *
+ * 2^-53 draw of the numpy Philox stream in *state (DEVICE), which is then
+ * advanced past the count draws -- bit-identical to rng.random(count) for the
+ * BRKGA populations (brkga.py:436-437 random init, :418 warm-start fill). */
+int vrp_random_fill(vrp_philox *state, int64_t count, double *out, void *stream);
+
 /* K5: ALNS repair, insertion.reinsert_all (insertion.py:484-516) on a fresh
  * InsertionContext of each partial solution, N independent instances.
  *   partial_ops[N][partial_stride] int32 + partial_lens[N][m]   (vehicle-major)

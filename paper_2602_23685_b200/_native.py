@@ -92,6 +92,7 @@ def declare_k4(L):
     L.vrp_alns_iterate.argtypes = [P, P, P, C.c_int32, P, P, P, P, P, i64, i64, i64, P, P, i64, P, P,
                                    i64, P]
     L.vrp_ls_build.argtypes = [P, C.c_int32, P, P, P, P, i64, P, i64, i64, P, C.c_int32, P, P]
+    L.vrp_random_fill.argtypes = [P, i64, P, P]
     for name in ("vrp_fitness_order", "vrp_evolve", "vrp_best_update", "vrp_repair_batch",
-                 "vrp_destroy_batch", "vrp_alns_iterate", "vrp_ls_build"):
+                 "vrp_destroy_batch", "vrp_alns_iterate", "vrp_ls_build", "vrp_random_fill"):
         getattr(L, name).restype = C.c_int

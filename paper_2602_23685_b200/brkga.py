@@ -338,6 +338,23 @@ def warm_start_seeds(instance, incumbent: Solution) -> list:
             encode(instance, _spt_solution(instance))]
 
 
+def warm_start_population_device(instance, alns_solution: Solution, params: BrkgaParams, rng) -> torch.Tensor:
+    """warm_start_population with the uniform fill drawn on the device
+    (vrp_random_fill); identical values and generator state, as a device
+    tensor for run_brkga."""
+    n_p = params.population
+    seeds = warm_start_seeds(instance, alns_solution)
+    while len(seeds) < WARM_SEED_COUNT:
+        seeds.append(perturb(seeds[0], rng))
+    n_warm = min(n_p, math.ceil(params.warm_start_fraction * n_p))
+    pop = R.random_device(rng, (n_p, 4 * instance.n))
+    rows = [seeds[slot] if slot < len(seeds) else perturb(seeds[slot % len(seeds)], rng)
+            for slot in range(n_warm)]
+    if rows:
+        pop[:n_warm] = torch.from_numpy(np.stack(rows)).to(pop.device)
+    return pop
+
+
 def warm_start_population(instance, alns_solution: Solution, params: BrkgaParams, rng) -> np.ndarray:
     """ceil(warm_start_fraction * N_p) warm slots cycling through 20 seeds
     (brkga.py:405-424), same draw order as the reference."""
@@ -363,13 +380,14 @@ def run_brkga(instance, params: BrkgaParams, warm_population=None, seed: int = 0
     (time.perf_counter() value, not in the reference) stops early at a
     generation boundary -- the time-budgeted pipeline uses it."""
     gen = R.as_philox(rng) if rng is not None else R.philox_generator(seed, R.BRKGA_STREAM)
-    if warm_population is not None:
-        host = np.array(warm_population, dtype=float, copy=True)
-    else:
-        host = random_population(instance.n, params.population, gen)
-    size, G = host.shape
     dev = torch.device("cuda", torch.cuda.current_device())
-    pop = torch.from_numpy(host).to(dev)
+    if isinstance(warm_population, torch.Tensor):
+        pop = warm_population.to(dev, torch.float64).clone()
+    elif warm_population is not None:
+        pop = torch.from_numpy(np.array(warm_population, dtype=float, copy=True)).to(dev)
+    else:  # rng.random((N_p, 4n)) (brkga.py:436-437), drawn on the device
+        pop = R.random_device(gen, (params.population, 4 * instance.n), dev)
+    size, G = pop.shape
     pop2 = torch.empty_like(pop)
     fits = torch.empty(size, dtype=torch.float64, device=dev)
     fits2 = torch.empty_like(fits)

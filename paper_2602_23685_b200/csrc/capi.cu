@@ -277,4 +277,12 @@ int vrp_ls_build(vrp_instance_t h, int32_t kind, const int32_t *base_ops, const 
                          "vrp_ls_build");
 }
 
+int vrp_random_fill(vrp_philox *state, int64_t count, double *out, void *stream) {
+    if (count < 0) return fail(VRP_EINVAL, "vrp_random_fill: count < 0%s");
+    if (count == 0) return 0;
+    if (!state || !out) return fail(VRP_EINVAL, "vrp_random_fill: null buffer%s");
+    return launch_result(launch_random_fill(state, count, out, static_cast<cudaStream_t>(stream)),
+                         "vrp_random_fill");
+}
+
 }  // extern "C"

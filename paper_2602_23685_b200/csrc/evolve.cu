@@ -212,6 +212,40 @@ __global__ void state_kernel(vrp_philox *__restrict__ Sp, EvolveShape sh,
     *Sp = S;
 }
 
+// Generator.random(count) (numpy: (next64 >> 11) * 2^-53, in order): thread b
+// produces Philox block b of the stream, thread 0 also the buffered head.
+__global__ void random_fill_kernel(const vrp_philox *__restrict__ Sp, int64_t count, double *__restrict__ out) {
+    const vrp_philox S = *Sp;
+    const int64_t head = 4 - (int64_t)S.buffer_pos;
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b == 0)
+        for (int64_t q = 0; q < head && q < count; ++q) out[q] = u64_to_double(S.buffer[S.buffer_pos + q]);
+    const int64_t base = head + 4 * b;
+    if (base >= count) return;
+    uint64_t c[4], o[4];
+    ctr_add(S.ctr, 1 + (uint64_t)b, c);
+    philox_block(c[0], c[1], c[2], c[3], S.key[0], S.key[1], o);
+    for (int j = 0; j < 4 && base + j < count; ++j) out[base + j] = u64_to_double(o[j]);
+}
+
+// advance the generator past Q next64 draws (random() leaves the u32 half alone)
+__global__ void advance_kernel(vrp_philox *__restrict__ Sp, uint64_t Q) {
+    vrp_philox S = *Sp;
+    const uint64_t head = 4 - (uint64_t)S.buffer_pos;
+    if (Q <= head) {
+        S.buffer_pos += (int32_t)Q;
+    } else {
+        const uint64_t qq = Q - head;
+        const uint64_t blocks = (qq + 3) / 4;
+        uint64_t c[4], buf[4];
+        ctr_add(S.ctr, blocks, c);
+        philox_block(c[0], c[1], c[2], c[3], S.key[0], S.key[1], buf);
+        for (int j = 0; j < 4; ++j) { S.ctr[j] = c[j]; S.buffer[j] = buf[j]; }
+        S.buffer_pos = (int32_t)(((qq - 1) & 3) + 1);
+    }
+    *Sp = S;
+}
+
 // (min fitness, first index) over fit[lo, hi); strict improvement of *best
 __global__ void __launch_bounds__(1024) best_kernel(const double *__restrict__ fit, int64_t lo, int64_t hi,
                                                     const double *__restrict__ genes, int64_t G,
@@ -316,5 +350,14 @@ int launch_best_update(const double *fit, int64_t lo, int64_t hi, const double *
                        double *best_fit, double *best_genes, int64_t *best_index, double *trace,
                        cudaStream_t stream) {
     best_kernel<<<1, 1024, 0, stream>>>(fit, lo, hi, genes, G, best_fit, best_genes, best_index, trace);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_random_fill(vrp_philox *state, int64_t count, double *out, cudaStream_t stream) {
+    if (count <= 0) return 0;
+    const int64_t blocks = (count + 3) / 4;
+    const int64_t grid = (blocks + 255) / 256;
+    random_fill_kernel<<<(unsigned)grid, 256, 0, stream>>>(state, count, out);
+    advance_kernel<<<1, 1, 0, stream>>>(state, (uint64_t)count);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
 }

@@ -27,6 +27,8 @@ int launch_best_update(const double *fit, int64_t lo, int64_t hi, const double *
                        double *best_fit, double *best_genes, int64_t *best_index, double *trace,
                        cudaStream_t stream);
 
+int launch_random_fill(vrp_philox *state, int64_t count, double *out, cudaStream_t stream);
+
 // repair.cu (K5)
 size_t repair_scratch_bytes(int n, int m);
 int launch_repair(const DevInstance &I, const int32_t *pops, int64_t pstride, const int32_t *plens,

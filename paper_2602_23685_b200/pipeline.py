@@ -93,7 +93,7 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_
     incumbent = best[1]
     if time.perf_counter() < t0 + seconds:
         rng = R.philox_generator(A.worker_seed(seed, 7001), R.BRKGA_STREAM)
-        pop = B.warm_start_population(instance, incumbent, brkga_params, rng)
+        pop = B.warm_start_population_device(instance, incumbent, brkga_params, rng)
         sol, _ = B.run_brkga(instance, brkga_params, warm_population=pop, seed=A.worker_seed(seed, 7002),
                              deadline=t0 + seconds)
         z = evaluate(instance, sol).makespan

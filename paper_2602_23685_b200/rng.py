@@ -80,3 +80,17 @@ def state_to_device(gen: np.random.Generator, device=None) -> torch.Tensor:
 
 def state_from_device(gen: np.random.Generator, t: torch.Tensor) -> None:
     set_state_bytes(gen, t.detach().cpu().numpy())
+
+
+def random_device(gen: np.random.Generator, shape, device=None) -> torch.Tensor:
+    """``gen.random(shape)`` generated on the device (vrp_random_fill): the
+    same doubles in the same order, and ``gen`` advanced exactly as numpy
+    would advance it."""
+    from . import _native as N
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    count = int(np.prod(shape))
+    out = torch.empty(tuple(shape), dtype=torch.float64, device=dev)
+    st = state_to_device(gen, dev)
+    N.check(N.lib().vrp_random_fill(N.ptr(st), count, N.ptr(out), N.stream_handle()), "vrp_random_fill")
+    state_from_device(gen, st)
+    return out

@@ -134,3 +134,34 @@ def test_single_island_equals_run_brkga():
     assert st.global_best == stats.best_fitness
     res = IS.islands_solution(inst, params, genes)
     assert res.solution == best
+
+
+@pytest.mark.parametrize("skip", [0, 1, 3, 5])
+def test_random_device_matches_numpy(skip):
+    """vrp_random_fill == Generator(Philox).random, from any buffer position
+    and with a pending u32 half (untouched by random())."""
+    from paper_2602_23685_b200 import rng as R
+    g1 = np.random.Generator(np.random.Philox(key=(31, 7)))
+    g2 = np.random.Generator(np.random.Philox(key=(31, 7)))
+    for g in (g1, g2):
+        g.random(skip)
+        g.integers(0, 1000)  # leaves a pending u32 half
+    for shape in ((3,), (17, 5), (1000, 3)):
+        a = R.random_device(g1, shape).cpu().numpy()
+        b = g2.random(shape)
+        np.testing.assert_array_equal(a, b)
+        assert np.array_equal(R.state_bytes(g1), R.state_bytes(g2))
+
+
+def test_warm_start_population_device_matches_host():
+    from paper_2602_23685_b200 import alns as A
+    inst = config_instance("eil51")
+    inc = A.construct_initial(inst)
+    prm = B.BrkgaParams(population=300, generations=1)
+    g1 = np.random.Generator(np.random.Philox(key=(5, 5)))
+    g2 = np.random.Generator(np.random.Philox(key=(5, 5)))
+    a = B.warm_start_population_device(inst, inc, prm, g1).cpu().numpy()
+    b = B.warm_start_population(inst, inc, prm, g2)
+    np.testing.assert_array_equal(a, b)
+    from paper_2602_23685_b200 import rng as R
+    assert np.array_equal(R.state_bytes(g1), R.state_bytes(g2))
