@@ -68,3 +68,34 @@ def test_product_path_fails_loudly_without_gpu():
     inst = Instance(n=1, d=((0, 10), (10, 0)), p=(0, 20), fleet=FleetConfig(1, 1), label="t")
     with pytest.raises(_native.NativeUnavailable):
         exact_makespan(inst, Solution.from_lists([[(1, "D"), (1, "P")]]))
+
+
+def test_struct_layouts_match_python_mirrors(tmp_path):
+    """sizeof / offsetof of the header's structs (compiled with gcc) equal the
+    numpy dtypes and ctypes structures the Python side packs them with."""
+    from paper_2602_23685_b200 import device as DV
+    from paper_2602_23685_b200 import rng as R
+    src = tmp_path / "sz.c"
+    fields = ["z", "z_best", "temperature", "t_init", "weights", "scores", "attempts", "stagnation",
+              "accepted", "rejected", "reheats", "best_it", "n_trace", "n_rows"]
+    pfields = [f for f, _ in DV.AlnsParamsC._fields_]
+    body = ['#include <stdio.h>', '#include <stddef.h>', '#include "vrp_rpd.h"', 'int main(void) {',
+            'printf("%zu %zu %zu\\n", sizeof(vrp_philox), sizeof(vrp_alns_worker), sizeof(vrp_alns_params));']
+    body += [f'printf("%zu\\n", offsetof(vrp_alns_worker, {f}));' for f in fields]
+    body += [f'printf("%zu\\n", offsetof(vrp_alns_params, {f}));' for f in pfields]
+    body += ['printf("%zu %zu %zu\\n", offsetof(vrp_philox, buffer_pos), offsetof(vrp_philox, has_uint32), '
+             'offsetof(vrp_philox, uinteger));', 'return 0; }']
+    src.write_text("\n".join(body))
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", f"-I{REPO / 'include'}", str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()
+    vals = [int(x) for x in out]
+    assert vals[:3] == [R._DTYPE.itemsize, DV.ALNS_WORKER_DTYPE.itemsize, ctypes.sizeof(DV.AlnsParamsC)]
+    k = 3
+    for f in fields:
+        assert vals[k] == DV.ALNS_WORKER_DTYPE.fields[f][1], f
+        k += 1
+    for f in pfields:
+        assert vals[k] == getattr(DV.AlnsParamsC, f).offset, f
+        k += 1
+    assert vals[k:] == [R._DTYPE.fields[f][1] for f in ("buffer_pos", "has_uint32", "uinteger")]
