@@ -47,13 +47,25 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(
 // Per candidate: ready table, plus (validating modes) an op bitmap and (two-
 // pass) the (route, position) of every dropoff.
 struct CandLayout {
-    size_t ready, bits, posd, total;
+    size_t ready, vals, freem, bits, posd, total;
 };
 
-__host__ __device__ inline CandLayout cand_layout(int n, int mode, int ready_bytes = 8) {
+// COMPACT: ready[] becomes a u8 slot id per customer (0xFF = not dropped) into
+// SLOTS uint32 ready values (see makespan_kernel).
+constexpr int SLOTS = 32;  // ready slots per candidate
+
+__host__ __device__ inline CandLayout cand_layout(int n, int mode, int ready_bytes = 8, bool compact = false) {
     CandLayout L;
     size_t o = 0;
-    L.ready = o; o += align16((size_t)ready_bytes * (size_t)(n + 1));
+    L.ready = o;
+    if (compact) {  // u8 slot id per customer + SLOTS ready values
+        o += align16((size_t)(n + 1));
+        L.vals = o; o += align16(sizeof(uint32_t) * SLOTS);
+        L.freem = o;
+    } else {
+        o += align16((size_t)ready_bytes * (size_t)(n + 1));
+        L.vals = L.freem = 0;
+    }
     L.bits = o;  if (mode != MODE_EXACT) o += align16(sizeof(uint32_t) * (size_t)((2 * n + 31) / 32));
     L.posd = o;  if (mode == MODE_TWO) o += align16(sizeof(uint32_t) * (size_t)(n + 1));
     L.total = o;
@@ -147,7 +159,20 @@ struct RouteStream {
 // twice the resident candidates.  Times are still computed in int64; a value
 // that does not fit marks the candidate ST_RETRY and the launcher re-runs just
 // those candidates with the 64-bit table (`fixup`), so results stay exact.
-template <typename OpT, bool INTD, int MODE, bool REC, bool NARROW>
+//
+// COMPACT (with NARROW, when m*k <= SLOTS): resources are conserved, so at
+// any point of any replay order the customers whose dropoff is done and
+// pickup is not number sum_v (q0_v - load_v) <= sum_v lo_v <= m*k for a
+// capacity-feasible candidate.  The ready table then needs only SLOTS values:
+// the candidate's free-slot mask is a register replicated over its lanes;
+// lanes dropping in the same iteration take the lowest free slots in lane
+// order (ballot rank), record the slot in a u8-per-customer map, and pickups
+// read the map, then the value, and return the slot (a rotation OR over the
+// candidate's lanes).  ~1.3 KB instead of 4 KB per candidate at n = 999, so
+// residency is set by registers, not shared memory.  A candidate that runs
+// out of slots is capacity-infeasible (status CAPACITY regardless) -- or,
+// should that reasoning ever fail, goes to the 64-bit fix-up pass (ST_RETRY).
+template <typename OpT, bool INTD, int MODE, bool REC, bool NARROW, bool COMPACT = false>
 __global__ void __launch_bounds__(256)
 makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 const int32_t *__restrict__ lens, int64_t N, int G, double *__restrict__ z_out,
@@ -161,7 +186,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     const int n = I.n, m = I.m, k = I.k, two_n = 2 * n;
     using TT = TimeT<INTD>;
     using RT = typename std::conditional<NARROW, uint32_t, TT>::type;
-    const CandLayout CL = cand_layout(n, MODE, (int)sizeof(RT));
+    const CandLayout CL = cand_layout(n, MODE, (int)sizeof(RT), COMPACT);
     TT *s_p = reinterpret_cast<TT *>(smem);
     unsigned char *wbase = smem + block_p_bytes(n) + (size_t)warp * G * CL.total;
 
@@ -171,6 +196,8 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     const int leader = g * m;  // lane holding route 0 of this lane's candidate
     unsigned char *cbase = wbase + (size_t)(glane ? g : 0) * CL.total;
     RT *s_ready = reinterpret_cast<RT *>(cbase + CL.ready);
+    uint8_t *s_sid = cbase + CL.ready;
+    uint32_t *s_val = reinterpret_cast<uint32_t *>(cbase + CL.vals);
     uint32_t *s_posd = reinterpret_cast<uint32_t *>(cbase + CL.posd);
 
     for (int c = threadIdx.x; c <= n; c += blockDim.x)
@@ -199,8 +226,13 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
 
         // ---- shared tables: ready = -1 (dropoff not done); validation bitmap
         for (int gg = 0; gg < G; ++gg) {
-            RT *rd = reinterpret_cast<RT *>(wbase + (size_t)gg * CL.total + CL.ready);
-            for (int c = lane; c <= n; c += 32) rd[c] = NARROW ? (RT)NOT_READY32 : (RT)-1;
+            if (COMPACT) {
+                uint32_t *sd = reinterpret_cast<uint32_t *>(wbase + (size_t)gg * CL.total + CL.ready);
+                for (int w = lane; w < (n + 4) / 4; w += 32) sd[w] = 0xFFFFFFFFu;
+            } else {
+                RT *rd = reinterpret_cast<RT *>(wbase + (size_t)gg * CL.total + CL.ready);
+                for (int c = lane; c <= n; c += 32) rd[c] = NARROW ? (RT)NOT_READY32 : (RT)-1;
+            }
             if (MODE != MODE_EXACT) {
                 uint32_t *bt = reinterpret_cast<uint32_t *>(wbase + (size_t)gg * CL.total + CL.bits);
                 for (int w = lane; w < (two_n + 31) / 32; w += 32) bt[w] = 0u;
@@ -269,19 +301,58 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 rs.advance(I);
             }
         } else {
+            // COMPACT: the free-slot mask (replicated over the candidate's lanes) and
+            // the rotation partners of its OR: after step s lane v holds v .. v+2^s-1 (mod m)
+            unsigned freem = ~0u;
+            const int pt1 = glane ? leader + (v + 1) % m : lane, pt2 = glane ? leader + (v + 2) % m : lane;
+            const int pt4 = glane ? leader + (v + 4) % m : lane, pt8 = glane ? leader + (v + 8) % m : lane;
+            const int pt16 = glane ? leader + (v + 16) % m : lane;
             for (;;) {
                 const bool active = run && !dead && rs.i < rs.L;
                 const int op = active ? rs.o[0] : 0;
                 const int c = op_customer(op);
                 const bool pick = op & 1;
-                const RT rraw = s_ready[c];
-                const TT r = NARROW ? (rraw == (RT)NOT_READY32 ? (TT)-1 : (TT)rraw) : (TT)rraw;
+                TT r;
+                int sid = 0xFF;
+                if (COMPACT) {
+                    sid = s_sid[c];
+                    r = (pick && sid != 0xFF) ? (TT)s_val[sid] : (TT)-1;
+                } else {
+                    const RT rraw = s_ready[c];
+                    r = NARROW ? (rraw == (RT)NOT_READY32 ? (TT)-1 : (TT)rraw) : (TT)rraw;
+                }
                 const TT pc = s_p[c];
                 const bool go = active && !(pick && r < (TT)0);
                 const TT arr = t + rs.leg0();
                 const TT tn = (pick && !(arr >= r)) ? r : arr;
+                int slot = SLOTS;
+                if (COMPACT) {
+                    const unsigned dm = __ballot_sync(VRP_FULL_MASK, go && !pick) & gmask;
+                    unsigned x = freem;
+                    const int below = __popc(dm & lanemask_lt());
+                    for (int q = 0, kq = __popc(dm); q < kq && x; ++q) {  // rank -> lowest free slots
+                        if (q == below && go && !pick) slot = __ffs(x) - 1;
+                        x &= x - 1;
+                    }
+                    unsigned fr = (go && pick && sid < SLOTS) ? (1u << sid) : 0u;
+                    fr |= __shfl_sync(VRP_FULL_MASK, fr, pt1);
+                    if (m > 2) fr |= __shfl_sync(VRP_FULL_MASK, fr, pt2);
+                    if (m > 4) fr |= __shfl_sync(VRP_FULL_MASK, fr, pt4);
+                    if (m > 8) fr |= __shfl_sync(VRP_FULL_MASK, fr, pt8);
+                    if (m > 16) fr |= __shfl_sync(VRP_FULL_MASK, fr, pt16);
+                    freem = x | fr;
+                }
                 if (go) {
-                    if (!pick) {
+                    if (COMPACT) {
+                        if (!pick) {
+                            const TT rv = tn + pc;
+                            ovf |= slot >= SLOTS || (unsigned long long)rv >= (unsigned long long)NOT_READY32;
+                            if (slot < SLOTS) {
+                                s_val[slot] = (uint32_t)rv;
+                                s_sid[c] = (uint8_t)slot;
+                            }
+                        }
+                    } else if (!pick) {
                         const TT rv = tn + pc;
                         if (NARROW) {
                             ovf |= (unsigned long long)rv >= (unsigned long long)NOT_READY32;
@@ -346,8 +417,8 @@ struct Shape {
 };
 
 template <typename Kern>
-int plan(Kern kern, int n, int m, int mode, int ready_bytes, Shape &out) {
-    const size_t per_cand = cand_layout(n, mode, ready_bytes).total;
+int plan(Kern kern, int n, int m, int mode, int ready_bytes, bool compact, Shape &out) {
+    const size_t per_cand = cand_layout(n, mode, ready_bytes, compact).total;
     const size_t pbytes = block_p_bytes(n);
     const int gmax = 32 / m;
     long best = -1;
@@ -369,17 +440,17 @@ int plan(Kern kern, int n, int m, int mode, int ready_bytes, Shape &out) {
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)out.smem) == cudaSuccess ? 0 : -1;
 }
 
-template <typename OpT, bool INTD, int MODE, bool REC, bool NARROW>
+template <typename OpT, bool INTD, int MODE, bool REC, bool NARROW, bool COMPACT = false>
 int launch_t(const DevInstance &I, const void *ops, int64_t stride, const int32_t *lens,
              int64_t N, double *z, int32_t *status, double *returns, int32_t *bottleneck,
              double *arrival, double *timev, int32_t *q0, cudaStream_t stream, int sm_count,
              int fixup) {
-    auto kern = makespan_kernel<OpT, INTD, MODE, REC, NARROW>;
+    auto kern = makespan_kernel<OpT, INTD, MODE, REC, NARROW, COMPACT>;
     static int cached_n = -1, cached_m = -1;
     static Shape sh;
     if (cached_n != I.n || cached_m != I.m) {
         using RT = typename std::conditional<NARROW, uint32_t, TimeT<INTD>>::type;
-        const int rc = plan(kern, I.n, I.m, MODE, (int)sizeof(RT), sh);
+        const int rc = plan(kern, I.n, I.m, MODE, (int)sizeof(RT), COMPACT, sh);
         if (rc) return rc;
         cached_n = I.n;
         cached_m = I.m;
@@ -401,7 +472,12 @@ template <typename OpT, int MODE>
 int launch_narrow(const DevInstance &I, const void *ops, int64_t stride, const int32_t *lens,
                   int64_t N, double *z, int32_t *status, double *returns, int32_t *bottleneck,
                   cudaStream_t stream, int sm_count) {
-    int rc = launch_t<OpT, true, MODE, false, true>(I, ops, stride, lens, N, z, status, returns, bottleneck,
+    int rc;
+    if (I.m * I.k <= SLOTS)  // slot table (see makespan_kernel: COMPACT)
+        rc = launch_t<OpT, true, MODE, false, true, true>(I, ops, stride, lens, N, z, status, returns, bottleneck,
+                                                          nullptr, nullptr, nullptr, stream, sm_count, 0);
+    else
+        rc = launch_t<OpT, true, MODE, false, true>(I, ops, stride, lens, N, z, status, returns, bottleneck,
                                                     nullptr, nullptr, nullptr, stream, sm_count, 0);
     if (rc) return rc;
     return launch_t<OpT, true, MODE, false, false>(I, ops, stride, lens, N, z, status, returns, bottleneck,
