@@ -184,7 +184,9 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     const int warp = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int n = I.n, m = I.m, k = I.k, two_n = 2 * n;
-    using TT = TimeT<INTD>;
+    // NARROW: event times in uint32 (every value the narrow table can hold);
+    // a wrap-around is detected and sends the candidate to the 64-bit pass
+    using TT = typename std::conditional<NARROW, uint32_t, TimeT<INTD>>::type;
     using RT = typename std::conditional<NARROW, uint32_t, TT>::type;
     const CandLayout CL = cand_layout(n, MODE, (int)sizeof(RT), COMPACT);
     TT *s_p = reinterpret_cast<TT *>(smem);
@@ -313,17 +315,21 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 const int c = op_customer(op);
                 const bool pick = op & 1;
                 TT r;
+                bool rdy;  // a pickup's dropoff has happened (dropoffs: always)
                 int sid = 0xFF;
                 if (COMPACT) {
                     sid = s_sid[c];
-                    r = (pick && sid != 0xFF) ? (TT)s_val[sid] : (TT)-1;
+                    rdy = !pick || sid != 0xFF;
+                    r = (TT)s_val[sid & (SLOTS - 1)];
                 } else {
                     const RT rraw = s_ready[c];
-                    r = NARROW ? (rraw == (RT)NOT_READY32 ? (TT)-1 : (TT)rraw) : (TT)rraw;
+                    r = (TT)rraw;
+                    rdy = NARROW ? (!pick || rraw != (RT)NOT_READY32) : !(pick && r < (TT)0);
                 }
                 const TT pc = s_p[c];
-                const bool go = active && !(pick && r < (TT)0);
-                const TT arr = t + rs.leg0();
+                const bool go = active && rdy;
+                const TT arr = t + (TT)rs.leg0();
+                if (NARROW) ovf |= arr < t;  // uint32 wrap
                 const TT tn = (pick && !(arr >= r)) ? r : arr;
                 int slot = SLOTS;
                 if (COMPACT) {
@@ -346,7 +352,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                     if (COMPACT) {
                         if (!pick) {
                             const TT rv = tn + pc;
-                            ovf |= slot >= SLOTS || (unsigned long long)rv >= (unsigned long long)NOT_READY32;
+                            ovf |= slot >= SLOTS || rv < tn || rv == (TT)NOT_READY32;
                             if (slot < SLOTS) {
                                 s_val[slot] = (uint32_t)rv;
                                 s_sid[c] = (uint8_t)slot;
@@ -355,7 +361,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                     } else if (!pick) {
                         const TT rv = tn + pc;
                         if (NARROW) {
-                            ovf |= (unsigned long long)rv >= (unsigned long long)NOT_READY32;
+                            ovf |= rv < tn || rv == (TT)NOT_READY32;
                             s_ready[c] = (RT)rv;
                         } else {
                             s_ready[c] = (RT)rv;
@@ -389,7 +395,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
 
         double ret = 0.0;
         if (live && st == ST_OK && L > 0) {
-            if (INTD) ret = (double)(t + (TT)__ldg(I.d32 + (int64_t)lastc * I.W));
+            if (INTD) ret = (double)((long long)t + (long long)__ldg(I.d32 + (int64_t)lastc * I.W));
             else ret = (double)t + __ldg(I.d + (int64_t)lastc * I.W);
         }
         double z = 0.0;  // returns are >= 0; empty routes count as 0
