@@ -309,6 +309,8 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             const int pt1 = glane ? leader + (v + 1) % m : lane, pt2 = glane ? leader + (v + 2) % m : lane;
             const int pt4 = glane ? leader + (v + 4) % m : lane, pt8 = glane ? leader + (v + 8) % m : lane;
             const int pt16 = glane ? leader + (v + 16) % m : lane;
+            unsigned cls = 0;  // this route's slot class {v, v+m, v+2m, ...}
+            for (int q = v; q < SLOTS; q += m) cls |= 1u << q;
             for (;;) {
                 const bool active = run && !dead && rs.i < rs.L;
                 const int op = active ? rs.o[0] : 0;
@@ -333,20 +335,33 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 const TT tn = (pick && !(arr >= r)) ? r : arr;
                 int slot = SLOTS;
                 if (COMPACT) {
-                    const unsigned dm = __ballot_sync(VRP_FULL_MASK, go && !pick) & gmask;
-                    unsigned x = freem;
-                    const int below = __popc(dm & lanemask_lt());
-                    for (int q = 0, kq = __popc(dm); q < kq && x; ++q) {  // rank -> lowest free slots
-                        if (q == below && go && !pick) slot = __ffs(x) - 1;
-                        x &= x - 1;
+                    // a dropping lane takes the lowest free slot of its own class
+                    // (slots = v mod m), so lanes never collide; if some lane's class
+                    // is exhausted, every dropping lane of the warp takes the
+                    // rank-th lowest free slot of its candidate instead (rare)
+                    const bool dgo = go && !pick;
+                    const unsigned mine = freem & cls;
+                    if (dgo && mine) slot = __ffs(mine) - 1;
+                    if (__any_sync(VRP_FULL_MASK, dgo && !mine)) {
+                        const unsigned dm = __ballot_sync(VRP_FULL_MASK, dgo) & gmask;
+                        unsigned x = freem;
+                        const int below = __popc(dm & lanemask_lt());
+                        slot = SLOTS;
+                        for (int q = 0, kq = __popc(dm); q < kq && x; ++q) {
+                            if (q == below && dgo) slot = __ffs(x) - 1;
+                            x &= x - 1;
+                        }
                     }
-                    unsigned fr = (go && pick && sid < SLOTS) ? (1u << sid) : 0u;
-                    fr |= __shfl_sync(VRP_FULL_MASK, fr, pt1);
-                    if (m > 2) fr |= __shfl_sync(VRP_FULL_MASK, fr, pt2);
-                    if (m > 4) fr |= __shfl_sync(VRP_FULL_MASK, fr, pt4);
-                    if (m > 8) fr |= __shfl_sync(VRP_FULL_MASK, fr, pt8);
-                    if (m > 16) fr |= __shfl_sync(VRP_FULL_MASK, fr, pt16);
-                    freem = x | fr;
+                    // slots taken (were free) and returned by pickups (were taken)
+                    // flip; the XOR of all of them is one OR over the candidate's lanes
+                    unsigned tg = (dgo && slot < SLOTS) ? (1u << slot) : 0u;
+                    if (go && pick && sid < SLOTS) tg |= 1u << sid;
+                    tg |= __shfl_sync(VRP_FULL_MASK, tg, pt1);
+                    if (m > 2) tg |= __shfl_sync(VRP_FULL_MASK, tg, pt2);
+                    if (m > 4) tg |= __shfl_sync(VRP_FULL_MASK, tg, pt4);
+                    if (m > 8) tg |= __shfl_sync(VRP_FULL_MASK, tg, pt8);
+                    if (m > 16) tg |= __shfl_sync(VRP_FULL_MASK, tg, pt16);
+                    freem ^= tg;
                 }
                 if (go) {
                     if (COMPACT) {
