@@ -309,8 +309,9 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             const int pt1 = glane ? leader + (v + 1) % m : lane, pt2 = glane ? leader + (v + 2) % m : lane;
             const int pt4 = glane ? leader + (v + 4) % m : lane, pt8 = glane ? leader + (v + 8) % m : lane;
             const int pt16 = glane ? leader + (v + 16) % m : lane;
-            unsigned cls = 0;  // this route's slot class {v, v+m, v+2m, ...}
+            unsigned cls = 0, cls_next = 0;  // slot classes {v, v+m, ...} of this and the next route
             for (int q = v; q < SLOTS; q += m) cls |= 1u << q;
+            for (int q = (v + 1) % m; q < SLOTS; q += m) cls_next |= 1u << q;
             for (;;) {
                 const bool active = run && !dead && rs.i < rs.L;
                 const int op = active ? rs.o[0] : 0;
@@ -341,8 +342,20 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                     // rank-th lowest free slot of its candidate instead (rare)
                     const bool dgo = go && !pick;
                     const unsigned mine = freem & cls;
-                    if (dgo && mine) slot = __ffs(mine) - 1;
-                    if (__any_sync(VRP_FULL_MASK, dgo && !mine)) {
+                    const bool own = dgo && mine;
+                    if (own) slot = __ffs(mine) - 1;
+                    const bool need = dgo && !mine;
+                    bool stuck = false;
+                    if (__any_sync(VRP_FULL_MASK, need)) {
+                        // borrow from the next route's class: its lowest free slot, or
+                        // the second lowest when that route takes its own lowest now
+                        const bool nxt_own = __shfl_sync(VRP_FULL_MASK, own, pt1);
+                        const unsigned nx = freem & cls_next;
+                        const unsigned cand = nxt_own ? (nx & (nx - 1)) : nx;
+                        if (need && cand) slot = __ffs(cand) - 1;
+                        stuck = need && !cand;
+                    }
+                    if (__any_sync(VRP_FULL_MASK, stuck)) {
                         const unsigned dm = __ballot_sync(VRP_FULL_MASK, dgo) & gmask;
                         unsigned x = freem;
                         const int below = __popc(dm & lanemask_lt());
