@@ -249,8 +249,16 @@ def run_gpu(args):
     from paper_2602_23685_b200.configs import config_instance
 
     rank, world, local = dist_env()
+    # VRP_BENCH_SHARE_GPU=1 (code-path test only): ranks share the visible
+    # GPUs round-robin over gloo -- never used for a reported number
+    shared = os.environ.get("VRP_BENCH_SHARE_GPU") == "1"
+    if shared:
+        local = local % torch.cuda.device_count()
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     inst = config_instance(CONFIG)
@@ -293,6 +301,9 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
+    # integral exact K1 = the narrow/compact pass + the 64-bit fix-up pass
+    # (csrc/makespan.cu launch_narrow); non-integral instances launch one kernel
+    launches_per_step = 2 if D.device_instance(inst).integral else 1
     total_units = n_cand * world
     value = total_units * args.steps / (ms / 1e3)
 
@@ -371,7 +382,7 @@ def run_gpu(args):
                            f"({n_cand * 2 * n * 2 / 1e9:.1f} GB ops per GPU), no flush",
                            "parallelism": f"candidate sharding x{world}"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": args.steps, "clocks": clk.summary(),
+                "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
                 "setup_s": round(setup_s, 2)}
         if not args.no_extra and world == 1:
             line["extra"] = extra_rates(dev, ops, lens, decode_ms, n_cand, args.pipeline_seconds)
