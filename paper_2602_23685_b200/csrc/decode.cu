@@ -176,6 +176,8 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
                 const int op = valid ? s_pend[j] : 0;
                 const int c = op_customer(op);
                 const bool pk = op & 1;
+                // the op's hint gene, loaded with the window (off the placement chain)
+                const double gj = valid ? __ldg(g + two_n + op) : 0.0;
                 unsigned todo = __ballot_sync(VRP_FULL_MASK, valid);
                 __syncwarp();
                 while (todo) {
@@ -193,7 +195,7 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
                     const double rf = __shfl_sync(VRP_FULL_MASK, r, f);
                     const int cf = op_customer(opf);
                     const bool pickf = opf & 1;
-                    const double gene = __ldg(g + two_n + opf);
+                    const double gene = __shfl_sync(VRP_FULL_MASK, gj, f);
                     double comp = 0.0;
                     bool fv = false;
                     if (vlane) {
