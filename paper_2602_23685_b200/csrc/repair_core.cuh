@@ -90,10 +90,10 @@ __host__ __device__ inline Layout make_layout(int n, int m) {
     L.s_hi_suf = take(4ull * (C + 1));
     L.s_drops = take(4ull * (C + 1));
     L.s_misc = take(8ull * (2 * m + 4));  // L, ret, exit_leg, sum_ret, omax[m]
-    L.s_ready = take(8ull * (n + 1));
-    L.s_has = take(4ull * (n + 1));
-    L.s_pv = take(4ull * (n + 1));
-    L.s_pi = take(4ull * (n + 1));
+    L.s_ready = take(8ull * C);  // per route position (+1 slot for the inserted customer)
+    L.s_has = take(4ull * C);
+    L.s_pv = take(4ull * C);
+    L.s_pi = take(4ull * C);
     L.gl_g = take(4ull * C);
     L.gl_ret = take(8ull * C);
     L.gl_stale = take(4ull * C);
@@ -660,9 +660,12 @@ __device__ void insert_op(Ctx &X, int v, int gap, int op) {  // one lane
     X.Lr[v] += 1;
 }
 
-// tentative_drop save / restore (insertion.py:326-347), warp-wide copies
+// tentative_drop save / restore (insertion.py:326-347), warp-wide copies.
+// pass1 on route v only rewrites the per-customer entries of v's dropoffs and
+// of the inserted customer c, so only those are saved (by route position; c
+// at position L) -- O(L) instead of O(n) per tentative drop.
 template <bool SAVE>
-__device__ void swap_state(Ctx &X, int v) {
+__device__ void swap_state(Ctx &X, int v, int c) {
     const int L = SAVE ? X.Lr[v] : (int)X.s_misc[0];
     const size_t o = (size_t)v * X.C, o1 = (size_t)v * (X.C + 1);
     for (int i = X.lane; i <= L; i += 32) {
@@ -678,9 +681,17 @@ __device__ void swap_state(Ctx &X, int v) {
             X.lo_suf[o1 + i] = X.s_lo_suf[i]; X.hi_suf[o1 + i] = X.s_hi_suf[i]; X.drops[o1 + i] = X.s_drops[i];
         }
     }
-    for (int c = X.lane; c <= X.n; c += 32) {
-        if (SAVE) { X.s_ready[c] = X.ready[c]; X.s_has[c] = X.has_ready[c]; X.s_pv[c] = X.pos_v[c]; X.s_pi[c] = X.pos_i[c]; }
-        else { X.ready[c] = X.s_ready[c]; X.has_ready[c] = X.s_has[c]; X.pos_v[c] = X.s_pv[c]; X.pos_i[c] = X.s_pi[c]; }
+    for (int i = X.lane; i <= L; i += 32) {
+        int cu;
+        if (i < L) {
+            const int op = SAVE ? X.seq[o + i] : X.s_seq[i];
+            if (op & 1) continue;
+            cu = opc(op);
+        } else {
+            cu = c;
+        }
+        if (SAVE) { X.s_ready[i] = X.ready[cu]; X.s_has[i] = X.has_ready[cu]; X.s_pv[i] = X.pos_v[cu]; X.s_pi[i] = X.pos_i[cu]; }
+        else { X.ready[cu] = X.s_ready[i]; X.has_ready[cu] = X.s_has[i]; X.pos_v[cu] = X.s_pv[i]; X.pos_i[cu] = X.s_pi[i]; }
     }
     if (X.lane == 0) {
         if (SAVE) {
@@ -735,7 +746,7 @@ __device__ int customer_options(Ctx &X, int c, PhiloxGen *gen, bool use_rng) {
         const int d_stale = X.keys[di].stale, g_drop = X.keys[di].a;
         __syncwarp();
         // tentative_drop: save, insert D, rebuild route vd only
-        swap_state<true>(X, vd);
+        swap_state<true>(X, vd, c);
         if (SCAN) {
             insert_op_warp(X, vd, g_drop, 2 * (c - 1));
             pass1_warp(X, vd);
@@ -763,7 +774,7 @@ __device__ int customer_options(Ctx &X, int c, PhiloxGen *gen, bool use_rng) {
             pk = X.keys[pi];
         }
         __syncwarp();
-        swap_state<false>(X, vd);  // restore
+        swap_state<false>(X, vd, c);  // restore
         if (np) {
             if (lane == 0) X.opts[nopt] = Opt{pk.cost, pk.stale, vd, g_drop, pk.a, pk.b, 0};
             ++nopt;
