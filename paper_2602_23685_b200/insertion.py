@@ -68,15 +68,16 @@ def reinsert_batch(instance, partial_ops, partial_lens, removed_lists, regret_ks
         rem[i, :len(r)] = r
         nrem[i] = len(r)
     states = None
-    if gens is not None:
+    if gens is not None:  # one H2D / D2H for all generator states
         gens = [R.as_philox(g) for g in gens]
-        states = torch.stack([R.state_to_device(g) for g in gens])
+        states = torch.from_numpy(np.stack([R.state_bytes(g) for g in gens])).to(
+            torch.device("cuda", torch.cuda.current_device()))
     out = Dev.repair_batch(instance, partial_ops, partial_lens, rem, nrem,
                            np.asarray(regret_ks, np.int32), states=states, stream=stream)
     if gens is not None:
-        host = states.cpu()
+        host = states.cpu().numpy()
         for i, g in enumerate(gens):
-            R.state_from_device(g, host[i])
+            R.set_state_bytes(g, host[i])
     return out["ops"].cpu().numpy(), out["lens"].cpu().numpy(), out["status"].cpu().numpy()
 
 
