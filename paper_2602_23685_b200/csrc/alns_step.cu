@@ -605,6 +605,9 @@ alns_kernel(DevInstance I, vrp_alns_params P, vrp_alns_worker *__restrict__ work
 
     int32_t *cur = cur_ops + (int64_t)w * 2 * n, *clen = cur_lens + (int64_t)w * m;
     int32_t *best = best_ops + (int64_t)w * 2 * n, *blen = best_lens + (int64_t)w * m;
+#ifdef VRP_PHASE_TIMERS
+    long long tph[6] = {0, 0, 0, 0, 0, 0};  // destroy, rebuild, repair, replay, removed, options calls
+#endif
     PhiloxGen gen;
     if (lane == 0) {
         S = workers[w];
@@ -634,6 +637,12 @@ alns_kernel(DevInstance I, vrp_alns_params P, vrp_alns_worker *__restrict__ work
             if (lane < m) D.off[lane] = o;
             __syncwarp();
         }
+#ifdef VRP_PHASE_TIMERS
+        long long tq = clock64();
+#define VRP_TICK(j) do { const long long t2 = clock64(); tph[j] += t2 - tq; tq = t2; } while (0)
+#else
+#define VRP_TICK(j) do {} while (0)
+#endif
         // destroy + remove_customers (alns.py:574; insertion.py:379-397)
         if (SCAN) {
             destroy_ool<INTD>(I, dop, q, P.q_min, cur, clen, D, C, lane, gen);
@@ -642,17 +651,25 @@ alns_kernel(DevInstance I, vrp_alns_params P, vrp_alns_worker *__restrict__ work
             destroy<INTD>(I, dop, q, P.q_min, cur, clen, D, C, lane, gen);
             remove_flagged(X, cur, clen, D);
         }
+        VRP_TICK(0);
         // repair (alns.py:258-274): reinsert_all, then exact_makespan
         rebuild_all<SCAN>(X);
         const int nrem = compact_flags(X, D.flag);
         const int rk = rop == 0 ? 0 : rop == 1 ? 2 : rop == 2 ? 3 : m;
+        VRP_TICK(1);
         int st = reinsert_core<SCAN>(X, nrem, rk, &gen, true);
+        VRP_TICK(2);
         double zc = 0.0;
         if (!st) {
             const int *row = X.seq + (size_t)(lane < m ? lane : 0) * C;
             const int L = lane < m ? X.Lr[lane] : 0;
             st = SCAN ? replay_ool<INTD>(I, row, L, lane, D, &zc) : replay<INTD>(I, row, L, lane, D, false, false, &zc);
         }
+        VRP_TICK(3);
+#ifdef VRP_PHASE_TIMERS
+        tph[4] += nrem;
+        tph[5] += (long long)nrem * (nrem + 1) / 2;
+#endif
         // acceptance + bookkeeping (alns.py:577-611)
         int acc = 0, nb = 0;
         if (lane == 0) {
@@ -721,6 +738,9 @@ alns_kernel(DevInstance I, vrp_alns_params P, vrp_alns_worker *__restrict__ work
     if (lane == 0) {
         S.rng = gen.s;
         workers[w] = S;
+#ifdef VRP_PHASE_TIMERS  // debug builds: phase clocks into the trace buffer
+        for (int j = 0; j < 6 && j < trace_cap; ++j) trace_z[(int64_t)w * trace_cap + j] = (double)tph[j];
+#endif
     }
 }
 

@@ -8,6 +8,6 @@ cp -r /root/repo/paper_2602_23685_b200/csrc $d/paper_2602_23685_b200/
 cp -r /root/repo/include $d/
 sed -i "$expr" $d/paper_2602_23685_b200/csrc/makespan.cu
 mkdir -p /root/repo/variants
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC -shared \
+nvcc $EXTRA -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC -shared \
      -I$d/include $d/paper_2602_23685_b200/csrc/*.cu -o /root/repo/variants/lib$name.so
 rm -rf $d
