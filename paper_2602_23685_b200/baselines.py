@@ -19,6 +19,8 @@ budget.  Candidates evaluated past the accepted one are speculation the
 reference never sees, so the result is bit-identical."""
 from __future__ import annotations
 
+import time
+
 import numpy as np
 import torch
 
@@ -48,8 +50,10 @@ def _phase_entries(kind, lens, n):
 
 
 def two_opt_improve(instance, solution: Solution, move_budget: int | None = None,
-                    chunk: int = CHUNK) -> Solution:
-    """First-improvement 2-opt / relocate / swap polish (baselines.py:372-455)."""
+                    chunk: int = CHUNK, deadline: float | None = None) -> Solution:
+    """First-improvement 2-opt / relocate / swap polish (baselines.py:372-455).
+    ``deadline`` (time.perf_counter() value; not in the reference) stops the
+    search between chunks -- the time-budgeted pipeline uses it."""
     n = instance.n
     budget = move_budget if move_budget is not None else 50 * n
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -72,6 +76,9 @@ def two_opt_improve(instance, solution: Solution, move_budget: int | None = None
             start_t = torch.from_numpy(starts).to(dev)
             pos = 0
             while pos < total and budget > 0:
+                if deadline is not None and time.perf_counter() >= deadline:
+                    budget = 0
+                    break
                 k = min(chunk, total - pos, budget)
                 c_ops, c_lens = _build(instance, kind, ops_t, lens_t, ent_t, start_t, pos, k,
                                        op_dtype=torch.int32)

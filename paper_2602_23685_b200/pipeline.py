@@ -35,29 +35,59 @@ def run_pipeline(instance, alns_params: A.AlnsParams, brkga_params: B.BrkgaParam
 def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_size: int = 296,
                         alns_params: A.AlnsParams | None = None,
                         brkga_params: B.BrkgaParams | None = None, seed: int = 0,
-                        initial: Solution | None = None, fit_cooling: bool = True):
+                        initial: Solution | None = None, fit_cooling: bool = True,
+                        polish: bool = True, polish_share: float | None = None, final_share: float = 0.1,
+                        alns_max_n: int = 400):
     """Best makespan found within a wall-clock budget (the BASELINE metric's
     'best makespan at fixed time'; the reference has no budget).
 
-    Stage 1, ``alns_share`` of the budget: ``pool_size`` device-resident ALNS
-    workers (one warp each, vrp_alns_iterate) in pools of
-    ``workers_per_pool`` that poll their pool's incumbent.  With
-    ``fit_cooling`` the SA schedule is fitted to the budget: a 10-iteration
+    Stage 0 (``polish``): the device first-improvement polish
+    (baselines.two_opt_improve: 2-opt / relocate / swap neighbourhoods scored
+    by K1 at tens of millions of candidates per second) takes the
+    constructed solution to a local optimum -- capped at ``polish_share`` of
+    the budget (default 0.4 for n >= 90; small instances measured better
+    when ALNS starts from the constructed solution, so 0 there).
+    Stage 1, ``alns_share`` of what remains before the final reserve (only
+    for n <= ``alns_max_n``: at larger n an ALNS iteration takes seconds):
+    ``pool_size`` device-resident ALNS workers (one warp each,
+    vrp_alns_iterate) in pools that poll their pool's incumbent.  With
+    ``fit_cooling`` the SA schedule is fitted to the stage: a 10-iteration
     calibration stretch measures the iteration rate, and the cooling rate is
-    set so that the temperature falls to 1e-3 of its start by the end of the
-    stage (the reference's alpha = 0.9998 assumes 20,000 iterations).
-    Stage 2, the rest: one BRKGA run (device generation loop) warm-started
-    from the ALNS incumbent, stopped at the deadline.
+    set so that the temperature falls to 1e-3 of its start by the end
+    (the reference's alpha = 0.9998 assumes 20,000 iterations).
+    Stage 2: one BRKGA run (device generation loop) warm-started from the
+    incumbent, stopped at its deadline.
+    Stage 3 (``polish``), the last ``final_share``: polish of the incumbent.
     Returns (best Solution, best makespan, trace [(seconds, best)])."""
+    from . import baselines as BL
     t0 = time.perf_counter()
+    end = t0 + seconds
     brkga_params = brkga_params or B.BrkgaParams(population=8192, generations=10**6)
     trace = []
     init = initial if initial is not None else A.construct_initial(instance, seed)
     z0 = evaluate(instance, init).makespan
     best = (z0, init)
     trace.append((time.perf_counter() - t0, z0))
-    alns_end = t0 + alns_share * seconds
-    if alns_params is None:
+
+    def offer(sol):
+        nonlocal best
+        z = evaluate(instance, sol).makespan
+        if z < best[0]:
+            best = (z, sol)
+            trace.append((time.perf_counter() - t0, z))
+
+    if polish_share is None:
+        polish_share = 0.4 if instance.n >= 90 else 0.0
+    if polish and polish_share > 0 and time.perf_counter() < end:
+        offer(BL.two_opt_improve(instance, best[1], move_budget=10**15,
+                                 deadline=min(end, t0 + polish_share * seconds)))
+    final_start = end - (final_share * seconds if polish else 0.0)
+    now = time.perf_counter()
+    alns_end = now + alns_share * max(0.0, final_start - now)
+    if instance.n > alns_max_n:
+        alns_end = now
+    init = best[1]
+    if alns_params is None and now < alns_end:
         alns_params = A.AlnsParams(max_iter=10)
         if fit_cooling:  # calibration stretch: iteration time of this pool on this instance
             probe = [A._Worker(instance, alns_params, A.worker_seed(seed + 1, i), init, None, None, i)
@@ -72,7 +102,7 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_
                                        best_check_interval=check, pool_sync_interval=check)
         else:
             alns_params = A.AlnsParams(max_iter=200_000)
-    if alns_params.max_iter and time.perf_counter() < alns_end:
+    if alns_params is not None and alns_params.max_iter and time.perf_counter() < alns_end:
         wpp = alns_params.workers_per_pool
         n_pools = (pool_size + wpp - 1) // wpp
         pools = [A._PoolShare() for _ in range(n_pools)]
@@ -90,14 +120,12 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_
             return time.perf_counter() >= alns_end
 
         A._DeviceWorkers(instance, alns_params, workers).drive(stop=stop, max_stretch=25)
-    incumbent = best[1]
-    if time.perf_counter() < t0 + seconds:
+    if time.perf_counter() < final_start:
         rng = R.philox_generator(A.worker_seed(seed, 7001), R.BRKGA_STREAM)
-        pop = B.warm_start_population_device(instance, incumbent, brkga_params, rng)
+        pop = B.warm_start_population_device(instance, best[1], brkga_params, rng)
         sol, _ = B.run_brkga(instance, brkga_params, warm_population=pop, seed=A.worker_seed(seed, 7002),
-                             deadline=t0 + seconds)
-        z = evaluate(instance, sol).makespan
-        if z < best[0]:
-            best = (z, sol)
-            trace.append((time.perf_counter() - t0, z))
+                             deadline=final_start)
+        offer(sol)
+    if polish and time.perf_counter() < end:
+        offer(BL.two_opt_improve(instance, best[1], move_budget=10**15, deadline=end))
     return best[1], best[0], trace
