@@ -11,8 +11,7 @@ from paper_2602_23685_b200.pipeline import run_pipeline_budget  # noqa: E402
 
 key, secs = sys.argv[1], float(sys.argv[2])
 inst = configs.config_instance(key)
-variants = [{}, {"polish_share": 0.0}, {"polish": False}] + [dict(v) for v in
-            ({"polish_share": 0.0, "alns_share": 0.5}, {"polish_share": 0.0, "final_share": 0.2})]
+variants = [{}] + [dict(v) for v in ({"final_share": 0.95}, {"final_share": 0.5}, {"alns_max_n": 50})]
 for kw in variants:
     t = time.perf_counter()
     sol, z, trace = run_pipeline_budget(inst, seconds=secs, **kw)

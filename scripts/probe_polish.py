@@ -10,8 +10,9 @@ inst = configs.config_instance(key)
 sol = A.construct_initial(inst)
 z0 = evaluate(inst, sol).makespan
 for secs in map(float, sys.argv[2:]):
-    t1 = time.perf_counter()
-    out = BL.two_opt_improve(inst, sol, move_budget=10**12, chunk=1 << 16, deadline=t1 + secs)
-    torch.cuda.synchronize()
-    print(f"{key}: initial {z0:.0f} -> polished {evaluate(inst, out).makespan:.0f} in "
-          f"{time.perf_counter() - t1:.1f}s (deadline {secs}s)", flush=True)
+    for resume in (False, True):
+        t1 = time.perf_counter()
+        out = BL.two_opt_improve(inst, sol, move_budget=10**12, deadline=t1 + secs, resume=resume)
+        torch.cuda.synchronize()
+        print(f"{key}: initial {z0:.0f} -> polished {evaluate(inst, out).makespan:.0f} in "
+              f"{time.perf_counter() - t1:.1f}s (deadline {secs}s, resume={resume})", flush=True)
