@@ -1,18 +1,20 @@
 """ALNS with simulated annealing -- drop-in for the reference's ``vrp_rpd.alns``
 (``/root/reference/pkg/src/vrp_rpd/alns.py``).
 
-Where the work goes:
-  repair             K5 (csrc/repair.cu) through insertion.reinsert_batch
-  candidate scoring  K1 exact_makespan / K2 two_pass_estimate (csrc/makespan.cu)
-  local search       pickup_repositioning / cross_agent_relocation candidates
-                     are scored in one K2 batch, the best 10 re-scored in one K1
-                     batch (alns.py:401-487)
-  destroy            host (small next to repair); numpy draws in
-                     the reference's order so one generator drives destroy (host)
-                     and repair (device) exactly like the reference's single rng
-  run_pool           all workers advance in lockstep; each iteration repairs
-                     every worker's candidate in ONE K5 launch and scores them
-                     in ONE K1 launch (the "ALNS candidate batch")
+Where the work goes (engine="device", the default):
+  iterations         csrc/alns_step.cu (vrp_alns_iterate): one warp per worker
+                     runs roulette, destroy (K6), remove_customers, repair (the
+                     K5 core), the exact replay, SA acceptance, cooling, reheat
+                     and weight updates for a whole stretch of iterations
+  local search       pickup_repositioning / cross_agent_relocation at their
+                     cadence, batched over all workers (localsearch.py:
+                     device-built neighbourhoods, K2 estimate, K1 verify)
+  pool sharing       on the host at the stretch boundaries, in the sequential
+                     loop's (iteration, worker) order
+engine="host" keeps destroy and acceptance on the host with one batched K5 +
+K1 launch per iteration (the cross-check of the device engine).  Both follow
+the reference's draw order, so one generator per worker behaves exactly like
+the reference's single rng.
 
 RNG: ``run_alns(seed)`` uses ``Generator(Philox(key=(seed, ALNS_STREAM)))``
 where the reference uses PCG64(seed) (see rng.py); with that substitution the
