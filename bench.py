@@ -210,6 +210,25 @@ def extra_rates(device, ops, lens, decode_ms, n_dec, pipeline_seconds=30.0):
     dw.run(6, 100)
     torch.cuda.synchronize()
     out["alns_iterations_per_s_eil51_1184_workers"] = 1184 * 95 / (time.perf_counter() - t0)
+    # K1 on the other benchmark configs (decoded candidates, device-resident)
+    for key in ("eil51", "kroA100", "a280"):
+        ki = config_instance(key)
+        cnt = 1 << 19
+        kops = torch.empty((cnt, 2 * ki.n), dtype=torch.int16, device=device)
+        klens = torch.empty((cnt, ki.m), dtype=torch.int32, device=device)
+        kg = torch.Generator(device=device).manual_seed(11)
+        for s0 in range(0, cnt, 1 << 16):
+            gg = torch.rand((1 << 16, 4 * ki.n), dtype=torch.float64, device=device, generator=kg)
+            D.decode_batch(ki, gg, out={"ops": kops[s0:s0 + (1 << 16)], "lens": klens[s0:s0 + (1 << 16)]})
+        res = {}
+        D.makespan_batch(ki, kops, klens, mode=0, out=res)
+        e0.record()
+        for _ in range(3):
+            D.makespan_batch(ki, kops, klens, mode=0, out=res)
+        e1.record()
+        torch.cuda.synchronize()
+        out[f"k1_evals_per_s_{key}"] = 3 * cnt / (e0.elapsed_time(e1) / 1e3)
+        del kops, klens
     if pipeline_seconds > 0:
         # BASELINE's "best makespan at fixed time": the whole ALNS -> BRKGA
         # pipeline (pipeline.run_pipeline_budget) on the kroA100 pipeline config
