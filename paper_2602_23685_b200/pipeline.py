@@ -191,3 +191,18 @@ def _kick_and_polish(instance, start: Solution, deadline: float, seed: int, batc
         if zp < zcur:
             cur, zcur = pol, zp
             yield pol
+
+
+def run_pipeline_budget_distributed(instance, seconds: float, seed: int = 0, group=None, **kw):
+    """run_pipeline_budget on every rank of ``group`` (one GPU each; SURVEY
+    §8(e): the pipeline's work shards as independent searches) with
+    rank-specific seeds, followed by a min-all-reduce of the best makespan
+    and a broadcast of the winner's routes (alns.sync_pool_share: lowest
+    rank wins ties).  Every rank returns (best Solution, best makespan,
+    its own trace)."""
+    rank, _ = A._dist_world(group)
+    sol, z, trace = run_pipeline_budget(instance, seconds, seed=seed + 1009 * rank, **kw)
+    share = A._PoolShare()
+    share.offer(rank, z, sol)
+    A.sync_pool_share(instance, share, group)
+    return share.best_sol, share.best_z, trace

@@ -79,3 +79,25 @@ def test_run_pool_distributed_world2_on_one_gpu():
     assert n0 + n1 == 12 and n0 == 6
     assert z0 == z1 == b0 == b1 and s0 == s1  # every rank returns the global best
     assert z0 <= min(l0, l1)
+
+
+def _pipeline_case(rank, world):
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    import torch
+    torch.cuda.set_device(0)
+    from conftest import config_instance
+    from paper_2602_23685_b200.pipeline import run_pipeline_budget_distributed
+    from paper_2602_23685_b200.schedule import evaluate
+    inst = config_instance("gr17")
+    sol, z, trace = run_pipeline_budget_distributed(inst, seconds=3.0, pool_size=8)
+    return z, evaluate(inst, sol).makespan, min(b for _, b in trace), sol.to_arrays(inst.n)[0].tolist()
+
+
+@pytest.mark.gpu
+def test_pipeline_budget_distributed_world2_on_one_gpu():
+    out = run_world(_pipeline_case)
+    (z0, e0, own0, s0), (z1, e1, own1, s1) = out[0], out[1]
+    assert z0 == z1 == e0 == e1 and s0 == s1  # one global best everywhere
+    assert z0 == min(own0, own1)
