@@ -66,6 +66,7 @@ def two_opt_improve(instance, solution: Solution, move_budget: int | None = None
     n = instance.n
     budget = move_budget if move_budget is not None else 50 * n
     dev = torch.device("cuda", torch.cuda.current_device())
+    op_dtype = torch.int16 if 2 * n <= 32767 else torch.int32
     o, l = solution.to_arrays(n)
     ops_t = torch.from_numpy(np.ascontiguousarray(o[None, :2 * n])).to(dev)
     lens_t = torch.from_numpy(np.ascontiguousarray(l[None])).to(dev)
@@ -104,15 +105,18 @@ def two_opt_improve(instance, solution: Solution, move_budget: int | None = None
                     break
                 k = min(step, total - p, budget)
                 c_ops, c_lens = _build(instance, kind, ops_t, lens_t, ent_t, start_t, p, k,
-                                       op_dtype=torch.int32)
-                r = DV.makespan_batch(instance, c_ops, c_lens, mode=N.MODE_EVALUATE)
+                                       op_dtype=op_dtype)
+                # candidates are permutations of a valid solution, so evaluate()'s
+                # structural check never fires and K1's exact mode gives the same
+                # status and makespan (CAPACITY before DEADLOCK in both)
+                r = DV.makespan_batch(instance, c_ops, c_lens, mode=N.MODE_EXACT)
                 ok = (r["status"] == 0) & (r["z"] < best - 1e-9)
                 hit = torch.nonzero(ok)
                 if hit.numel():
                     j = int(hit[0, 0])
                     budget -= j + 1
                     best = float(r["z"][j])
-                    ops_t = c_ops[j:j + 1].clone()
+                    ops_t = c_ops[j:j + 1].to(torch.int32)
                     lens_t = c_lens[j:j + 1].clone()
                     improved = True
                     phase, pos, fruitless, step = ph, p + j + 1, 0, chunk

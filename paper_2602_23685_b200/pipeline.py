@@ -83,13 +83,13 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_
             trace.append((time.perf_counter() - t0, z))
 
     if polish_share is None:
-        polish_share = 0.4 if instance.n >= 90 else 0.0
+        polish_share = (0.4 if instance.n < 500 else 0.6) if instance.n >= 90 else 0.0
     if final_share is None:  # measured (profiles/r01_summary.md): the polish + kick tail
         final_share = 0.1 if instance.n < 90 else (0.5 if instance.n < 500 else 0.6)
     if polish and polish_share > 0 and time.perf_counter() < end:
-        # resumed scans converge ~3x faster at n ~ 1000 to a slightly weaker
-        # optimum; below that both converge in well under a second
-        offer(BL.two_opt_improve(instance, best[1], move_budget=10**15, resume=instance.n >= 500,
+        # (restarting scans: at n = 999 they converge in ~25 s to a better optimum
+        # than the resumed variant's ~10 s one; below that both take < 1 s)
+        offer(BL.two_opt_improve(instance, best[1], move_budget=10**15,
                                  deadline=min(end, t0 + polish_share * seconds)))
     final_start = end - (final_share * seconds if polish else 0.0)
     now = time.perf_counter()
@@ -161,8 +161,10 @@ def _kick_and_polish(instance, start: Solution, deadline: float, seed: int, batc
     rng = R.philox_generator(A.worker_seed(seed, 7100), R.ALNS_STREAM)
     cur, zcur = start, evaluate(instance, start).makespan
     dev = torch.device("cuda", torch.cuda.current_device())
-    qq = min(q, n)
-    while time.perf_counter() < deadline - 0.5:
+    qq = min(q if n < 500 else 2, n)  # removals cascade; large n: smaller kicks
+    kick_s = 0.0  # duration of the last kick step (repairs do not watch the clock)
+    while time.perf_counter() + 1.2 * kick_s < deadline - 0.5:
+        tk = time.perf_counter()
         o, l = cur.to_arrays(n)
         ops = torch.from_numpy(np.tile(o[:2 * n], (batch, 1))).to(dev)
         lens = torch.from_numpy(np.tile(l, (batch, 1))).to(dev)
@@ -186,6 +188,7 @@ def _kick_and_polish(instance, start: Solution, deadline: float, seed: int, batc
             continue
         k = ok[good[np.argmin(zs[good])]]
         kicked = Solution.from_arrays(ro[k], rl[k])
+        kick_s = time.perf_counter() - tk
         pol = BL.two_opt_improve(instance, kicked, move_budget=10**15, resume=True, deadline=deadline)
         zp = evaluate(instance, pol).makespan
         if zp < zcur:
