@@ -19,7 +19,7 @@ from paper_2602_23685_b200.schedule import Solution
 pytestmark = pytest.mark.gpu
 
 SHAPES = [(1, 1, 1), (1, 3, 1), (2, 1, 1), (2, 2, 1), (3, 5, 2), (4, 1, 3), (5, 2, 1), (6, 3, 2),
-          (8, 8, 1), (9, 2, 4), (12, 4, 2), (17, 3, 5)]
+          (8, 8, 1), (9, 2, 4), (12, 4, 2), (17, 3, 5), (20, 8, 5), (12, 7, 6)]  # last two: m*k > 32 (narrow K1)
 
 
 def _instance(n, m, k, seed, kind):
