@@ -36,17 +36,25 @@ def _phase_entries(kind, lens, n):
     """Entries + candidate counts of one neighbourhood (zero-count entries
     dropped so that entry_start stays strictly increasing)."""
     m = lens.size
+    L = np.asarray(lens, np.int64)
     if kind == 2:  # 2-opt: routes in order
-        ent = [(0, v, 0, 0, 0) for v in range(m) if lens[v] >= 2]
-        cnt = [int(lens[v]) * (int(lens[v]) - 1) // 2 for v in range(m) if lens[v] >= 2]
+        vs = np.flatnonzero(L >= 2)
+        ent = np.zeros((vs.size, 5), np.int32)
+        ent[:, 1] = vs
+        cnt = L[vs] * (L[vs] - 1) // 2
     elif kind == 0:  # relocation: every op in route order
-        off = np.concatenate([[0], np.cumsum(lens)[:-1]])
-        ent = [(0, v, i, int(off[v] + i), 0) for v in range(m) for i in range(int(lens[v]))]
-        cnt = [2 * n + m - 2] * len(ent)
+        total = int(L.sum())
+        off = np.cumsum(L) - L
+        v = np.repeat(np.arange(m), L)
+        ent = np.zeros((total, 5), np.int32)
+        ent[:, 1] = v
+        ent[:, 3] = np.arange(total)
+        ent[:, 2] = ent[:, 3] - off[v]
+        cnt = np.full(total, 2 * n + m - 2, np.int64)
     else:  # swap: one entry, all flat pairs
-        ent = [(0, 0, 0, 0, 0)]
-        cnt = [2 * n * (2 * n - 1) // 2]
-    return np.asarray(ent, np.int32).reshape(-1, 5), np.asarray(cnt, np.int64)
+        ent = np.zeros((1, 5), np.int32)
+        cnt = np.array([2 * n * (2 * n - 1) // 2], np.int64)
+    return ent, cnt
 
 
 def two_opt_improve(instance, solution: Solution, move_budget: int | None = None,
