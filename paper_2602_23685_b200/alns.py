@@ -31,7 +31,7 @@ from . import insertion
 from . import rng as R
 from .insertion import InsertionContext, RepairFailed
 from .schedule import (OpKind, ScheduleError, Solution, evaluate, exact_makespan,
-                       pack_solutions, two_pass_estimate)
+                       pack_solutions, two_pass_estimate)  # noqa: F401 (module attribute, as in the reference)
 
 _D, _P = OpKind.DROPOFF, OpKind.PICKUP
 
