@@ -275,9 +275,13 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             while (rs.i < rs.L) {
                 const int op = rs.o[0];
                 const int c = op_customer(op);
-                t = t + rs.leg0();
+                const TT tn = t + (TT)rs.leg0();
+                if (NARROW) ovf |= tn < t;  // uint32 wrap -> 64-bit fix-up pass
+                t = tn;
                 if (!(op & 1)) {
-                    s_ready[c] = t + s_p[c];
+                    const TT rv = t + s_p[c];
+                    if (NARROW) ovf |= rv < t;
+                    s_ready[c] = (RT)rv;
                     s_posd[c] = ((uint32_t)v << 16) | (uint32_t)rs.i;
                 }
                 cap_step(op, k, s, lo, hi);
@@ -293,9 +297,11 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             while (rs.i < rs.L) {
                 const int op = rs.o[0];
                 const int c = op_customer(op);
-                t = t + rs.leg0();
+                const TT tn = t + (TT)rs.leg0();
+                if (NARROW) ovf |= tn < t;
+                t = tn;
                 if (op & 1) {
-                    const TT r = s_ready[c];
+                    const TT r = (TT)s_ready[c];
                     if (r > t) t = r;
                     const uint32_t pd = s_posd[c];
                     dead |= (int)(pd >> 16) == v && (int)(pd & 0xffffu) > rs.i;
@@ -507,7 +513,7 @@ int launch_narrow(const DevInstance &I, const void *ops, int64_t stride, const i
                   int64_t N, double *z, int32_t *status, double *returns, int32_t *bottleneck,
                   cudaStream_t stream, int sm_count) {
     int rc;
-    if (I.m * I.k <= SLOTS)  // slot table (see makespan_kernel: COMPACT)
+    if (MODE != MODE_TWO && I.m * I.k <= SLOTS)  // slot table (see makespan_kernel: COMPACT)
         rc = launch_t<OpT, true, MODE, false, true, true>(I, ops, stride, lens, N, z, status, returns, bottleneck,
                                                           nullptr, nullptr, nullptr, stream, sm_count, 0);
     else
@@ -533,6 +539,9 @@ int dispatch_mode(const DevInstance &I, const void *ops, int64_t stride, const i
     if (INTD && mode == MODE_EVAL)
         return launch_narrow<OpT, MODE_EVAL>(I, ops, stride, lens, N, z, status, returns, bottleneck,
                                              stream, sm_count);
+    if (INTD && mode == MODE_TWO)  // the two-pass tables need every dropoff: narrow, not compact
+        return launch_narrow<OpT, MODE_TWO>(I, ops, stride, lens, N, z, status, returns, bottleneck,
+                                            stream, sm_count);
     switch (mode) {
         case MODE_EXACT:
             return launch_t<OpT, INTD, MODE_EXACT, false, false>(I, ops, stride, lens, N, z, status, returns,
