@@ -20,6 +20,8 @@
 #include <float.h>
 #include <limits.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -46,13 +48,15 @@ struct DecodeLayout {
     size_t pend, ready, total;
 };
 
-__host__ __device__ inline DecodeLayout decode_layout(int n) {
+__host__ __device__ inline DecodeLayout decode_layout(int n, int ready_bytes = 8) {
     DecodeLayout L;
     L.pend = 0;
     L.ready = align16(2 * (size_t)(2 * n));
-    L.total = L.ready + align16(8 * (size_t)(n + 1));
+    L.total = L.ready + align16((size_t)ready_bytes * (size_t)(n + 1));
     return L;
 }
+
+constexpr uint32_t NOT_DROPPED32 = 0xFFFFFFFFu;
 
 __device__ __forceinline__ uint64_t order_key(double x) {
     if (x != x) return 0xFFFFFFFFFFFFFFFEull;  // NaN: after every number
@@ -127,34 +131,42 @@ sort_kernel(const double *__restrict__ genes, int64_t gstride, int64_t N, int tw
     }
 }
 
-template <bool INTD, typename OutT>
+// NARROW (integral instances): the ready table holds uint32 (NOT_DROPPED32 =
+// not dropped) -- 8 KB instead of 12 KB per warp at n = 999, so more warps
+// per SM.  A ready time that does not fit sets retry[chrom]; the launcher's
+// second (wide, `only = retry`) pass re-decodes exactly those chromosomes.
+template <bool INTD, typename OutT, bool NARROW = false>
 __global__ void __launch_bounds__(256, 1)
 decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, int64_t N,
               int relax, double penalty, double *__restrict__ fitness_out,
               double *__restrict__ makespan_out, int32_t *__restrict__ scheduled_out,
               int64_t *__restrict__ visits_out, OutT *__restrict__ ops_out, int64_t ostride,
               int32_t *__restrict__ lens_out, const uint16_t *__restrict__ order,
-              uint32_t *__restrict__ seq_scratch) {
+              uint32_t *__restrict__ seq_scratch, uint8_t *__restrict__ retry,
+              const uint8_t *__restrict__ only) {
+    using RT = typename std::conditional<NARROW, uint32_t, double>::type;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int n = I.n, m = I.m, k = I.k, two_n = 2 * n;
-    const DecodeLayout Ly = decode_layout(n);
+    const DecodeLayout Ly = decode_layout(n, (int)sizeof(RT));
     unsigned char *base = smem + (size_t)warp * Ly.total;
-    volatile double *s_ready = reinterpret_cast<volatile double *>(base + Ly.ready);
+    volatile RT *s_ready = reinterpret_cast<volatile RT *>(base + Ly.ready);
     uint16_t *s_pend = reinterpret_cast<uint16_t *>(base + Ly.pend);
     const bool vlane = lane < m;
     const unsigned lt = lanemask_lt();
 
     for (int64_t chrom = (int64_t)blockIdx.x * wpb + warp; chrom < N;
          chrom += (int64_t)gridDim.x * wpb) {
+        if (only && !only[chrom]) continue;  // fix-up pass: just the flagged chromosomes
         const double *g = genes + chrom * gstride;
         uint32_t *seq = seq_scratch + chrom * (int64_t)two_n;  // (op | vehicle << 16) log
+        bool ovf = false;
         // ---- pending list = the stable priority order (sort_kernel)
         const uint16_t *ord = order + chrom * (int64_t)two_n;
         for (int i = lane; i < two_n; i += 32) s_pend[i] = __ldg(ord + i);
-        for (int c = lane; c <= n; c += 32) s_ready[c] = -1.0;  // -1: not dropped
+        for (int c = lane; c <= n; c += 32) s_ready[c] = NARROW ? (RT)NOT_DROPPED32 : (RT)-1.0;  // not dropped
         __syncwarp();
 
         // ---- vehicle state (lane v = vehicle v)
@@ -181,8 +193,10 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
                 unsigned todo = __ballot_sync(VRP_FULL_MASK, valid);
                 __syncwarp();
                 while (todo) {
-                    const double r = pk ? s_ready[c] : 0.0;
-                    const bool feas = pk ? (r >= 0.0 && any_pick && (relax || pick_maxT >= r)) : any_drop;
+                    const RT rr = pk ? s_ready[c] : (RT)0;
+                    const bool dropped = NARROW ? rr != (RT)NOT_DROPPED32 : (double)rr >= 0.0;
+                    const double r = (double)rr;
+                    const bool feas = pk ? (dropped && any_pick && (relax || pick_maxT >= r)) : any_drop;
                     const unsigned fm = __ballot_sync(VRP_FULL_MASK, feas) & todo;
                     const unsigned defm = fm ? (todo & ((1u << (__ffs(fm) - 1)) - 1u)) : todo;
                     if ((defm >> lane) & 1u) s_pend[nw + __popc(defm & lt)] = (uint16_t)op;
@@ -240,7 +254,15 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
                         ++cnt;
                     }
                     if (lane == 0) {
-                        if (!pickf) s_ready[cf] = cstar + __ldg(I.p + cf);
+                        if (!pickf) {
+                            const double rv = cstar + __ldg(I.p + cf);
+                            if (NARROW) {
+                                ovf |= !(rv < 4294967295.0);
+                                s_ready[cf] = (RT)(ovf ? 0.0 : rv);
+                            } else {
+                                s_ready[cf] = (RT)rv;
+                            }
+                        }
                         if (seq_scratch) seq[nseq] = (uint32_t)opf | ((uint32_t)vstar << 16);
                     }
                     ++nseq;
@@ -257,6 +279,7 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
         // ---- fitness (brkga.py:198-200): unused vehicles return at 0 + d[0][0]
         double ret = vlane ? t + dist<INTD>(I, loc, 0) : -DBL_MAX;
         const double z = warp_max(ret);
+        if (NARROW && lane == 0) retry[chrom] = ovf ? 1 : 0;
         if (lane == 0) {
             fitness_out[chrom] = z + penalty * (double)npend;
             if (makespan_out) makespan_out[chrom] = z;
@@ -293,12 +316,14 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
     }
 }
 
-template <bool INTD, typename OutT>
-int launch_t(const DevInstance &I, const double *genes, int64_t gstride, int64_t N, int relax,
+// one decode_kernel launch, occupancy planned once per (instantiation, n)
+template <bool INTD, typename OutT, bool NARROW>
+int launch_k(const DevInstance &I, const double *genes, int64_t gstride, int64_t N, int relax,
              double penalty, double *fitness, double *makespan, int32_t *scheduled, int64_t *visits,
-             void *ops_out, int64_t ostride, int32_t *lens_out, cudaStream_t stream, int sm_count) {
-    auto kern = decode_kernel<INTD, OutT>;
-    const size_t per_warp = decode_layout(I.n).total;
+             void *ops_out, int64_t ostride, int32_t *lens_out, const uint16_t *order, uint32_t *seq,
+             uint8_t *retry, const uint8_t *only, cudaStream_t stream, int sm_count) {
+    auto kern = decode_kernel<INTD, OutT, NARROW>;
+    const size_t per_warp = decode_layout(I.n, NARROW ? 4 : 8).total;
     static size_t cached_pw = 0;
     static int cached_w = 0, cached_blocks = 0;
     if (cached_pw != per_warp) {
@@ -317,13 +342,34 @@ int launch_t(const DevInstance &I, const double *genes, int64_t gstride, int64_t
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per_warp * best_w));
         cached_pw = per_warp; cached_w = best_w; cached_blocks = best_blocks;
     }
-    // scratch: priority order (u16) and, when the solution is wanted, the
-    // (op | vehicle << 16) event log
+    const size_t bytes = per_warp * (size_t)cached_w;
+    int64_t want = (N + cached_w - 1) / cached_w;
+    int64_t grid = (int64_t)cached_blocks * sm_count;
+    if (grid > want) grid = want;
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, 32 * cached_w, bytes, stream>>>(I, genes, gstride, N, relax, penalty, fitness,
+                                                         makespan, scheduled, visits,
+                                                         static_cast<OutT *>(ops_out), ostride, lens_out,
+                                                         order, seq, retry, only);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
+template <bool INTD, typename OutT>
+int launch_t(const DevInstance &I, const double *genes, int64_t gstride, int64_t N, int relax,
+             double penalty, double *fitness, double *makespan, int32_t *scheduled, int64_t *visits,
+             void *ops_out, int64_t ostride, int32_t *lens_out, cudaStream_t stream, int sm_count) {
+    // scratch: priority order (u16), the (op | vehicle << 16) event log when the
+    // solution is wanted, and (integral instances) the narrow pass's retry flags
     const int two_n = 2 * I.n;
     uint16_t *order = nullptr;
     uint32_t *seq = nullptr;
+    uint8_t *retry = nullptr;
     if (cudaMallocAsync(&order, sizeof(uint16_t) * (size_t)N * two_n, stream) != cudaSuccess) return -1;
     if (ops_out && cudaMallocAsync(&seq, sizeof(uint32_t) * (size_t)N * two_n, stream) != cudaSuccess) return -1;
+    // narrow tables only where shared memory limits residency (measured: below
+    // n ~ 500 the uint32 conversions cost more than the extra warps give)
+    const bool narrow = INTD && I.n >= 500;
+    if (narrow && cudaMallocAsync(&retry, (size_t)N, stream) != cudaSuccess) return -1;
     {
         static int sort_n = -1;
         const int sw = 4;
@@ -340,19 +386,24 @@ int launch_t(const DevInstance &I, const double *genes, int64_t gstride, int64_t
         if (sgrid > swant) sgrid = swant;
         sort_kernel<<<(unsigned)sgrid, 32 * sw, sbytes, stream>>>(genes, gstride, N, two_n, order);
     }
-    const size_t bytes = per_warp * (size_t)cached_w;
-    int64_t want = (N + cached_w - 1) / cached_w;
-    int64_t grid = (int64_t)cached_blocks * sm_count;
-    if (grid > want) grid = want;
-    if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, 32 * cached_w, bytes, stream>>>(I, genes, gstride, N, relax, penalty, fitness,
-                                                         makespan, scheduled, visits,
-                                                         static_cast<OutT *>(ops_out), ostride, lens_out,
-                                                         order, seq);
-    const cudaError_t e = cudaPeekAtLastError();
+    int rc;
+    if (narrow) {  // narrow pass, then the wide kernel over the (normally no) flagged chromosomes
+        rc = launch_k<INTD, OutT, true>(I, genes, gstride, N, relax, penalty, fitness, makespan, scheduled,
+                                        visits, ops_out, ostride, lens_out, order, seq, retry, nullptr, stream,
+                                        sm_count);
+        if (!rc)
+            rc = launch_k<INTD, OutT, false>(I, genes, gstride, N, relax, penalty, fitness, makespan,
+                                             scheduled, visits, ops_out, ostride, lens_out, order, seq,
+                                             nullptr, retry, stream, sm_count);
+    } else {
+        rc = launch_k<INTD, OutT, false>(I, genes, gstride, N, relax, penalty, fitness, makespan, scheduled,
+                                         visits, ops_out, ostride, lens_out, order, seq, nullptr, nullptr,
+                                         stream, sm_count);
+    }
     cudaFreeAsync(order, stream);
     if (seq) cudaFreeAsync(seq, stream);
-    return e == cudaSuccess ? 0 : -1;
+    if (retry) cudaFreeAsync(retry, stream);
+    return rc;
 }
 
 }  // namespace

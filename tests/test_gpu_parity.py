@@ -143,6 +143,13 @@ def test_narrow_ready_overflow_falls_back_exactly():
     genes = I.chromosomes(inst.n, 512, (17, 17))
     ref = O.decode_batch(inst, genes)
     small = O.decode_batch(base, genes)
+    # K3's narrow ready table overflows the same way: its wide fix-up pass must
+    # reproduce the oracle decode (int16 and int32 outputs)
+    for dt in (torch.int32, torch.int16):
+        r = dev().decode_batch(inst, _cuda(genes), op_dtype=dt)
+        np.testing.assert_array_equal(r["ops"].cpu().numpy().astype(np.int32), ref["ops"])
+        np.testing.assert_array_equal(r["fitness"].cpu().numpy(), ref["fitness"])
+        np.testing.assert_array_equal(r["visits"].cpu().numpy(), ref["visits"])
     for mode, name in ((0, "exact"), (1, "evaluate")):
         r = dev().makespan_batch(inst, _cuda(ref["ops"]), _cuda(ref["lens"]), mode=mode)
         z, st = O.makespan_batch(inst, ref["ops"], ref["lens"], mode=name)
