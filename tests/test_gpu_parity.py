@@ -158,3 +158,21 @@ def test_narrow_ready_overflow_falls_back_exactly():
         np.testing.assert_array_equal(r["z"].cpu().numpy(), z)
         r = dev().makespan_batch(base, _cuda(small["ops"]), _cuda(small["lens"]), mode=mode)
         np.testing.assert_array_equal(r["z"].cpu().numpy(), small["makespan"])
+
+
+def test_decode_narrow_overflow_at_large_n():
+    """n >= 500 decodes through K3's narrow (uint32) ready table; a scaled
+    dsj1000 instance pushes some ready times past 2^32, and the wide fix-up
+    pass must reproduce the oracle exactly for those and the narrow pass for
+    the rest."""
+    from paper_2602_23685_b200.instance import Instance
+    base = config_instance("dsj1000")
+    d, p = base.arrays()
+    inst = Instance.from_arrays(d * 5.0, p * 5.0, base.m, base.k, label="dsj-x5")
+    genes = I.chromosomes(inst.n, 64, (19, 19))
+    ref = O.decode_batch(inst, genes)
+    assert (ref["makespan"] > 2.0**32).any() and (ref["makespan"] < 2.0**32).any()
+    r = dev().decode_batch(inst, _cuda(genes), op_dtype=torch.int16)
+    np.testing.assert_array_equal(r["ops"].cpu().numpy().astype(np.int32), ref["ops"])
+    np.testing.assert_array_equal(r["fitness"].cpu().numpy(), ref["fitness"])
+    np.testing.assert_array_equal(r["visits"].cpu().numpy(), ref["visits"])
