@@ -493,64 +493,68 @@ __device__ __forceinline__ double cost_of(const Ctx &X, int v, double new_ret) {
 __device__ __forceinline__ int imax3(int a, int b, int c) { int x = a > b ? a : b; return x > c ? x : c; }
 __device__ __forceinline__ int imin3(int a, int b, int c) { int x = a < b ? a : b; return x < c ? x : c; }
 
-// insertion.py:193-242 (pair = false) and :244-272 (pair = true); warp-wide,
-// one gap per lane, compacted in gap order into gl_*; returns the count.
-__device__ int eval_gaps(Ctx &X, int v, int c, bool pick, bool pair) {
+// One insertion gap g of route v for customer c (insertion.py:193-272):
+// capacity interval, new return and stale count.  Returns feasibility.
+__device__ __forceinline__ bool gap_eval(const Ctx &X, int v, int g, int c, bool pick, bool pair, double ready_c,
+                                         double &new_ret, int &stale) {
     const int k = X.k, L = X.Lr[v];
     const size_t o = (size_t)v * X.C, o1 = (size_t)v * (X.C + 1);
     const int *sq = X.seq + o;
-    const double *T = X.T + o, *dep = X.dep + o, *M = X.M + o;
-    const int *sp = X.sp + o1, *lo_pre = X.lo_pre + o1, *hi_pre = X.hi_pre + o1;
-    const int *lo_suf = X.lo_suf + o1, *hi_suf = X.hi_suf + o1, *drops = X.drops + o1;
+    const double *T = X.T + o;
+    const int sp_g = X.sp[o1 + g];
+    const int ls = X.lo_suf[o1 + g], hs = X.hi_suf[o1 + g];
+    const int lp = X.lo_pre[o1 + g], hp = X.hi_pre[o1 + g];
+    int lo, hi;
+    if (pair) {
+        lo = imax3(lp, ls, 1 - sp_g);
+        hi = imin3(hp, hs, k - sp_g);
+    } else if (!pick) {
+        lo = imax3(lp, 1 - sp_g, ls == NEG_BIG ? NEG_BIG : ls + 1);
+        hi = imin3(hp, hs == POS_BIG ? POS_BIG : hs + 1, k);
+    } else {
+        lo = imax3(lp, ls == NEG_BIG ? NEG_BIG : ls - 1, 0);
+        hi = imin3(hp, k - 1 - sp_g, hs == POS_BIG ? POS_BIG : hs - 1);
+    }
+    new_ret = 0.0;
+    stale = 0;
+    if (lo > hi) return false;
+    const double prev_dep = g ? X.dep[o + g - 1] : 0.0;
+    const int prev_loc = g ? opc(sq[g - 1]) : 0;
+    double dep_x;
+    if (pair) {
+        dep_x = prev_dep + X.d(prev_loc, c) + X.p(c);
+    } else {
+        const double arr = prev_dep + X.d(prev_loc, c);
+        dep_x = (!pick || arr >= ready_c) ? arr : ready_c;
+    }
+    if (g == L) {
+        new_ret = dep_x + X.d(c, 0);
+    } else {
+        const double s_entry = dep_x + X.d(c, opc(sq[g]));
+        const double tail = s_entry - T[g];
+        const double mg = X.M[o + g];
+        if (pair) new_ret = T[L - 1] + (tail > mg ? tail : mg) + X.exit_leg[v];
+        else new_ret = (T[L - 1] + X.exit_leg[v]) + (tail > mg ? tail : mg);
+        const double old_entry = prev_dep + (T[g] - (g ? T[g - 1] : 0.0));
+        stale = s_entry > old_entry + 1e-12 ? X.drops[o1 + g] : 0;
+    }
+    return true;
+}
+
+// insertion.py:193-242 (pair = false) and :244-272 (pair = true); warp-wide,
+// one gap per lane, compacted in gap order into gl_*; returns the count.
+__device__ int eval_gaps(Ctx &X, int v, int c, bool pick, bool pair) {
+    const int L = X.Lr[v];
     const double ready_c = X.has_ready[c] ? X.ready[c] : 0.0;
     int min_gap = 0;
     if (pick && X.pos_v[c] == v && X.pos_i[c] + 1 > min_gap) min_gap = X.pos_i[c] + 1;
-    const double t_last = L ? T[L - 1] + X.exit_leg[v] : 0.0;
     const unsigned lt = lanemask_lt();
     int cnt = 0;
     for (int base = min_gap; base <= L; base += 32) {
         const int g = base + X.lane;
-        bool ok = g <= L;
         double new_ret = 0.0;
         int stale = 0;
-        if (ok) {
-            const int sp_g = sp[g];
-            const int ls = lo_suf[g], hs = hi_suf[g];
-            int lo, hi;
-            if (pair) {
-                lo = imax3(lo_pre[g], ls, 1 - sp_g);
-                hi = imin3(hi_pre[g], hs, k - sp_g);
-            } else if (!pick) {
-                lo = imax3(lo_pre[g], 1 - sp_g, ls == NEG_BIG ? NEG_BIG : ls + 1);
-                hi = imin3(hi_pre[g], hs == POS_BIG ? POS_BIG : hs + 1, k);
-            } else {
-                lo = imax3(lo_pre[g], ls == NEG_BIG ? NEG_BIG : ls - 1, 0);
-                hi = imin3(hi_pre[g], k - 1 - sp_g, hs == POS_BIG ? POS_BIG : hs - 1);
-            }
-            ok = lo <= hi;
-            if (ok) {
-                const double prev_dep = g ? dep[g - 1] : 0.0;
-                const int prev_loc = g ? opc(sq[g - 1]) : 0;
-                double dep_x;
-                if (pair) {
-                    dep_x = prev_dep + X.d(prev_loc, c) + X.p(c);
-                } else {
-                    const double arr = prev_dep + X.d(prev_loc, c);
-                    dep_x = (!pick || arr >= ready_c) ? arr : ready_c;
-                }
-                if (g == L) {
-                    new_ret = dep_x + X.d(c, 0);
-                } else {
-                    const double s_entry = dep_x + X.d(c, opc(sq[g]));
-                    const double tail = s_entry - T[g];
-                    const double mg = M[g];
-                    if (pair) new_ret = T[L - 1] + (tail > mg ? tail : mg) + X.exit_leg[v];
-                    else new_ret = t_last + (tail > mg ? tail : mg);
-                    const double old_entry = prev_dep + (T[g] - (g ? T[g - 1] : 0.0));
-                    stale = s_entry > old_entry + 1e-12 ? drops[g] : 0;
-                }
-            }
-        }
+        const bool ok = g <= L && gap_eval(X, v, g, c, pick, pair, ready_c, new_ret, stale);
         const unsigned mk = __ballot_sync(VRP_FULL_MASK, ok);
         if (ok) {
             const int at = cnt + __popc(mk & lt);
@@ -562,6 +566,49 @@ __device__ int eval_gaps(Ctx &X, int v, int c, bool pick, bool pair) {
     }
     __syncwarp();
     return cnt;
+}
+
+// The pickup gaps of every route in one warp pass (the P scan of a
+// tentative drop, insertion.py:456-466): flat gap index over the routes in
+// order, gaps ascending -- the order of m eval_gaps calls -- keyed straight
+// into keys[0..): (cost, d_stale + stale, vp, g).  Returns the count.
+__device__ int pick_keys_all(Ctx &X, int c, int d_stale) {
+    const int m = X.m, lane = X.lane;
+    int first = 0, cntv = 0;
+    if (lane < m) {
+        first = X.pos_v[c] == lane ? X.pos_i[c] + 1 : 0;
+        cntv = X.Lr[lane] + 1 - first;
+        if (cntv < 0) cntv = 0;
+    }
+    int ex = cntv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(VRP_FULL_MASK, ex, o);
+        if (lane >= o) ex += y;
+    }
+    const int total = __shfl_sync(VRP_FULL_MASK, ex, m - 1);
+    ex -= cntv;  // exclusive start of route `lane`
+    const double ready_c = X.has_ready[c] ? X.ready[c] : 0.0;
+    const unsigned lt = lanemask_lt();
+    int np = 0;
+    for (int base = 0; base < total; base += 32) {
+        const int F = base + lane;
+        int v = 0;
+        for (int u = 1; u < m; ++u) {  // the route holding flat gap F
+            const int eu = __shfl_sync(VRP_FULL_MASK, ex, u);
+            const int cu = __shfl_sync(VRP_FULL_MASK, cntv, u);
+            if (cu > 0 && F >= eu) v = u;
+        }
+        const int g = __shfl_sync(VRP_FULL_MASK, first, v) + (F - __shfl_sync(VRP_FULL_MASK, ex, v));
+        double new_ret = 0.0;
+        int stale = 0;
+        const bool ok = F < total && gap_eval(X, v, g, c, true, false, ready_c, new_ret, stale);
+        const unsigned mk = __ballot_sync(VRP_FULL_MASK, ok);
+        if (ok) X.keys[np + __popc(mk & lt)] = Key{cost_of(X, v, new_ret), d_stale + stale, v, g, 0};
+        np += __popc(mk);
+    }
+    __syncwarp();
+    return np;
 }
 
 // warp argmin of keys[0..cnt), excluding indices in `skip` (up to 3)
@@ -760,14 +807,7 @@ __device__ int customer_options(Ctx &X, int c, PhiloxGen *gen, bool use_rng) {
             refresh(X);
         }
         __syncwarp();
-        int np = 0;
-        for (int vp = 0; vp < m; ++vp) {
-            const int pc = eval_gaps(X, vp, c, true, false);
-            for (int i = lane; i < pc; i += 32)
-                X.keys[np + i] = Key{cost_of(X, vp, X.gl_ret[i]), d_stale + X.gl_stale[i], vp, X.gl_g[i], 0};
-            np += pc;
-            __syncwarp();
-        }
+        const int np = pick_keys_all(X, c, d_stale);
         Key pk{};
         if (np) {
             const int pi = pick_windowed(X.keys, np, lane, gen, use_rng);
