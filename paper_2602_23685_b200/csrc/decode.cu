@@ -1,10 +1,12 @@
 // decode.cu -- K3: BRKGA multi-pass decoder (brkga.py:92-207) over a batch
 // of chromosomes, one warp per chromosome.
 //
-//  sort    stable argsort of the 2n priority genes (brkga.py:116): bitonic
-//          network in shared memory over (order-preserving u64 key, index)
-//          pairs -- a strict total order, hence equal to numpy's stable sort
-//          (-0.0 is canonicalised to +0.0, NaN sorts last as in numpy).
+//  sort    stable argsort of the 2n priority genes (brkga.py:116) on the
+//          strict total order (order-preserving u64 key, index) -- equal to
+//          numpy's stable sort (-0.0 canonicalised to +0.0, NaN last): a
+//          bucketed counting sort with per-bucket insertion sorts, or, for a
+//          chromosome whose priorities cluster, a bitonic network in shared
+//          memory.
 //  decode  lane v = vehicle v holds (t, loc, net, lo, hi) in registers.  The
 //          pending list is scanned 32 ops at a time: a dropoff is deferred iff
 //          no vehicle can take one (the capacity test does not depend on the
@@ -110,7 +112,7 @@ __device__ __forceinline__ void fleet_flags(bool vlane, double t, int net, int l
 // per chromosome; writes the order as u16 op indices to order_out[N][2n].
 __global__ void __launch_bounds__(256)
 sort_kernel(const double *__restrict__ genes, int64_t gstride, int64_t N, int two_n,
-            uint16_t *__restrict__ order_out) {
+            uint16_t *__restrict__ order_out, const uint8_t *__restrict__ only) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     const int P2 = pow2_at_least(two_n);
@@ -118,6 +120,7 @@ sort_kernel(const double *__restrict__ genes, int64_t gstride, int64_t N, int tw
     uint64_t *s_key = reinterpret_cast<uint64_t *>(base);
     uint16_t *s_idx = reinterpret_cast<uint16_t *>(base + align16(8 * (size_t)P2));
     for (int64_t chrom = (int64_t)blockIdx.x * wpb + warp; chrom < N; chrom += (int64_t)gridDim.x * wpb) {
+        if (only && !only[chrom]) continue;  // fallback pass of bucket_sort_kernel
         const double *g = genes + chrom * gstride;
         for (int i = lane; i < P2; i += 32) {
             s_key[i] = i < two_n ? order_key(__ldg(g + i)) : ~0ull;
@@ -135,6 +138,106 @@ sort_kernel(const double *__restrict__ genes, int64_t gstride, int64_t N, int tw
 // not dropped) -- 8 KB instead of 12 KB per warp at n = 999, so more warps
 // per SM.  A ready time that does not fit sets retry[chrom]; the launcher's
 // second (wide, `only = retry`) pass re-decodes exactly those chromosomes.
+// Bucketed stable argsort (same order as sort_kernel): NB buckets monotone in
+// the key (x < 0 | [0,1) in NB-2 equal slices | >= 1, inf, NaN), counted and
+// scattered with shared atomics, then every bucket insertion-sorted by
+// (order key, index) -- O(n) for BRKGA's [0, 1) genes instead of the bitonic
+// network's O(n log^2 n).  A chromosome with a bucket of more than MAXB
+// entries (many equal or clustered priorities) is flagged for sort_kernel.
+constexpr int MAXB = 48;
+
+// bucket count: a power of two near n (about two priorities per bucket), 64..1024
+__host__ __device__ inline int bucket_count(int two_n) {
+    const int b = pow2_at_least(two_n / 2);
+    return b < 64 ? 64 : (b > 1024 ? 1024 : b);
+}
+
+__device__ __forceinline__ int bucket_of(double x, int nb) {
+    if (x < 0.0) return 0;
+    if (!(x < 1.0)) return nb - 1;  // >= 1, +inf, NaN
+    return 1 + (int)(x * (double)(nb - 2));
+}
+
+__host__ __device__ inline size_t bucket_sort_bytes(int n) {
+    return align16(4 * (size_t)bucket_count(2 * n)) + align16(2 * (size_t)(2 * n));
+}
+
+__global__ void __launch_bounds__(256)
+bucket_sort_kernel(const double *__restrict__ genes, int64_t gstride, int64_t N, int two_n,
+                   uint16_t *__restrict__ order_out, uint8_t *__restrict__ fallback) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    unsigned char *base = smem + (size_t)warp * bucket_sort_bytes(two_n / 2);
+    const int NB = bucket_count(two_n), PER = NB / 32;
+    int *cnt = reinterpret_cast<int *>(base);
+    uint16_t *out = reinterpret_cast<uint16_t *>(base + align16(4 * (size_t)NB));
+    const unsigned lt = lanemask_lt();
+    for (int64_t chrom = (int64_t)blockIdx.x * wpb + warp; chrom < N; chrom += (int64_t)gridDim.x * wpb) {
+        const double *g = genes + chrom * gstride;
+        for (int b = lane; b < NB; b += 32) cnt[b] = 0;
+        __syncwarp();
+        for (int i = lane; i < two_n; i += 32) atomicAdd(&cnt[bucket_of(__ldg(g + i), NB)], 1);
+        __syncwarp();
+        // exclusive prefix (lane owns NB/32 consecutive buckets) + largest bucket
+        int run = 0, big = 0;
+        for (int j = 0; j < PER; ++j) {
+            const int c = cnt[lane * PER + j];
+            run += c;
+            big = c > big ? c : big;
+        }
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(VRP_FULL_MASK, incl, o);
+            if (lane >= o) incl += y;
+        }
+        for (int o = 16; o; o >>= 1) {
+            const int y = __shfl_xor_sync(VRP_FULL_MASK, big, o);
+            big = y > big ? y : big;
+        }
+        if (big > MAXB) {  // clustered priorities: leave it to the bitonic pass
+            if (lane == 0) fallback[chrom] = 1;
+            __syncwarp();
+            continue;
+        }
+        int at = incl - run;
+        for (int j = 0; j < PER; ++j) {
+            const int c = cnt[lane * PER + j];
+            cnt[lane * PER + j] = at;  // bucket start, advanced by the scatter
+            at += c;
+        }
+        __syncwarp();
+        for (int i = lane; i < two_n; i += 32) {
+            const int pos = atomicAdd(&cnt[bucket_of(__ldg(g + i), NB)], 1);
+            out[pos] = (uint16_t)i;
+        }
+        __syncwarp();
+        // cnt[b] is now bucket b's end; sort each bucket by (key, index)
+        for (int b = lane; b < NB; b += 32) {
+            const int e = cnt[b], s0 = b ? cnt[b - 1] : 0;
+            for (int i = s0 + 1; i < e; ++i) {
+                const uint16_t xi = out[i];
+                const uint64_t kx = order_key(__ldg(g + xi));
+                int j = i - 1;
+                while (j >= s0) {
+                    const uint16_t yj = out[j];
+                    const uint64_t ky = order_key(__ldg(g + yj));
+                    if (ky < kx || (ky == kx && yj < xi)) break;
+                    out[j + 1] = yj;
+                    --j;
+                }
+                out[j + 1] = xi;
+            }
+        }
+        __syncwarp();
+        uint16_t *o = order_out + chrom * (int64_t)two_n;
+        for (int i = lane; i < two_n; i += 32) o[i] = out[i];
+        if (lane == 0) fallback[chrom] = 0;
+        __syncwarp();
+    }
+    (void)lt;
+}
+
 template <bool INTD, typename OutT, bool NARROW = false>
 __global__ void __launch_bounds__(256, 1)
 decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, int64_t N,
@@ -370,21 +473,33 @@ int launch_t(const DevInstance &I, const double *genes, int64_t gstride, int64_t
     // n ~ 500 the uint32 conversions cost more than the extra warps give)
     const bool narrow = INTD && I.n >= 500;
     if (narrow && cudaMallocAsync(&retry, (size_t)N, stream) != cudaSuccess) return -1;
+    uint8_t *fb = nullptr;
+    if (cudaMallocAsync(&fb, (size_t)N, stream) != cudaSuccess) return -1;
     {
-        static int sort_n = -1;
         const int sw = 4;
-        const size_t sbytes = sort_bytes(I.n) * sw;
+        static int bucket_n = -1, sort_n = -1;
+        const size_t bbytes = bucket_sort_bytes(I.n) * sw, sbytes = sort_bytes(I.n) * sw;
+        if (bucket_n != I.n) {
+            if (cudaFuncSetAttribute(bucket_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bbytes) != cudaSuccess)
+                return -1;
+            bucket_n = I.n;
+        }
         if (sort_n != I.n) {
             if (cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbytes) != cudaSuccess)
                 return -1;
             sort_n = I.n;
         }
-        int sblocks = 0;
+        const int64_t swant = (N + sw - 1) / sw;
+        int bblocks = 0, sblocks = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bblocks, bucket_sort_kernel, 32 * sw, bbytes);
+        int64_t bgrid = (int64_t)(bblocks > 0 ? bblocks : 1) * sm_count;
+        if (bgrid > swant) bgrid = swant;
+        bucket_sort_kernel<<<(unsigned)bgrid, 32 * sw, bbytes, stream>>>(genes, gstride, N, two_n, order, fb);
+        // the (normally few) chromosomes whose priorities cluster: bitonic network
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sblocks, sort_kernel, 32 * sw, sbytes);
         int64_t sgrid = (int64_t)(sblocks > 0 ? sblocks : 1) * sm_count;
-        const int64_t swant = (N + sw - 1) / sw;
         if (sgrid > swant) sgrid = swant;
-        sort_kernel<<<(unsigned)sgrid, 32 * sw, sbytes, stream>>>(genes, gstride, N, two_n, order);
+        sort_kernel<<<(unsigned)sgrid, 32 * sw, sbytes, stream>>>(genes, gstride, N, two_n, order, fb);
     }
     int rc;
     if (narrow) {  // narrow pass, then the wide kernel over the (normally no) flagged chromosomes
@@ -401,6 +516,7 @@ int launch_t(const DevInstance &I, const double *genes, int64_t gstride, int64_t
                                          stream, sm_count);
     }
     cudaFreeAsync(order, stream);
+    cudaFreeAsync(fb, stream);
     if (seq) cudaFreeAsync(seq, stream);
     if (retry) cudaFreeAsync(retry, stream);
     return rc;
