@@ -176,3 +176,27 @@ def test_decode_narrow_overflow_at_large_n():
     np.testing.assert_array_equal(r["ops"].cpu().numpy().astype(np.int32), ref["ops"])
     np.testing.assert_array_equal(r["fitness"].cpu().numpy(), ref["fitness"])
     np.testing.assert_array_equal(r["visits"].cpu().numpy(), ref["visits"])
+
+
+@pytest.mark.parametrize("key", ["eil51", "dsj1000"])
+def test_decode_sort_paths_clustered_priorities(key):
+    """K3's argsort: uniform priorities take the bucketed counting sort,
+    clustered ones (constant, a handful of distinct values, negative / >= 1
+    / NaN / -0.0 entries) overflow a bucket and take the bitonic fallback;
+    both must give numpy's stable order, hence the oracle's decode."""
+    inst = config_instance(key)
+    n2 = 2 * inst.n
+    g = I.philox(88, 1)
+    rows = [np.full(4 * inst.n, 0.5),                                   # one bucket
+            np.concatenate([g.integers(0, 4, n2) / 4.0, g.random(n2)]),  # 4 distinct values
+            np.concatenate([g.integers(0, 40, n2) / 40.0, g.random(n2)]),  # ~n/20 repeats each
+            g.random(4 * inst.n)]                                       # uniform
+    odd = g.random(4 * inst.n)
+    odd[:8] = [-0.0, 0.0, -1.5, 1.0, 2.0, np.inf, -np.inf, np.nan]
+    rows.append(odd)
+    genes = np.stack(rows)
+    r = dev().decode_batch(inst, _cuda(genes))
+    ref = O.decode_batch(inst, genes)
+    np.testing.assert_array_equal(r["ops"].cpu().numpy(), ref["ops"])
+    np.testing.assert_array_equal(r["fitness"].cpu().numpy(), ref["fitness"])
+    np.testing.assert_array_equal(r["visits"].cpu().numpy(), ref["visits"])
