@@ -191,7 +191,8 @@ def extra_rates(device, ops, lens, decode_ms, n_dec, pipeline_seconds=30.0):
         parts.append(o[:2 * inst.n]); plens.append(l); rem.append(r)
     parts, plens = np.stack(parts), np.stack(plens)
     rks = [(0, 2, 3, inst.m)[i % 4] for i in range(cnt)]
-    INS.reinsert_batch(inst, parts[:64], plens[:64], rem[:64], rks[:64], [I.philox(9, i) for i in range(64)])
+    # warm-up with the full batch (the first call of a size pays the scratch pool growth)
+    INS.reinsert_batch(inst, parts, plens, rem, rks, [I.philox(9, i) for i in range(cnt)])
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     INS.reinsert_batch(inst, parts, plens, rem, rks, [I.philox(9, i) for i in range(cnt)])
