@@ -133,3 +133,24 @@ def test_device_pool_equals_host_pool():
     assert b1 == b2 and i1["best_makespan"] == i2["best_makespan"]
     for a, b in zip(i1["worker_stats"], i2["worker_stats"]):
         _same_stats(a, b)
+
+
+def test_device_engine_equals_host_engine_fractional_instance():
+    """alns_kernel<false,false> (fp64 distances, one-lane passes): the device
+    engine equals the host engine on a non-integral instance."""
+    from paper_2602_23685_b200.instance import Instance
+    base = config_instance("eil51")
+    d, p = base.arrays()
+    g = np.random.default_rng(21)
+    d2 = d + g.random(d.shape) * 0.7
+    d2 = (d2 + d2.T) / 2
+    np.fill_diagonal(d2, 0.0)
+    p2 = p + g.random(p.shape) / 3
+    p2[0] = 0.0
+    inst = Instance.from_arrays(d2, p2, base.m, base.k, label="eil51-frac")
+    params = A.AlnsParams(max_iter=60, weight_interval=20, stagnation_threshold=15, t0=0.05)
+    initial = A.construct_initial(inst)
+    b1, s1 = A.run_alns(inst, params, seed=8, initial=initial, engine="device")
+    b2, s2 = A.run_alns(inst, params, seed=8, initial=initial, engine="host")
+    assert b1 == b2
+    _same_stats(s1, s2)
