@@ -259,6 +259,9 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
     uint16_t *s_pend = reinterpret_cast<uint16_t *>(base + Ly.pend);
     const bool vlane = lane < m;
     const unsigned lt = lanemask_lt();
+    int mhalf = 1;  // argmin butterfly over lanes [0, 2*mhalf) ⊇ the m vehicle lanes
+    while (2 * mhalf < m) mhalf <<= 1;
+    if (m == 1) mhalf = 0;
 
     for (int64_t chrom = (int64_t)blockIdx.x * wpb + warp; chrom < N;
          chrom += (int64_t)gridDim.x * wpb) {
@@ -291,8 +294,9 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
                 const int op = valid ? s_pend[j] : 0;
                 const int c = op_customer(op);
                 const bool pk = op & 1;
-                // the op's hint gene, loaded with the window (off the placement chain)
-                const double gj = valid ? __ldg(g + two_n + op) : 0.0;
+                // the op's hint vehicle, computed with the window (off the placement chain)
+                const int hj = valid ? hint_vehicle(m, __ldg(g + two_n + op)) : 0;
+                const double pj = valid && !pk ? __ldg(I.p + c) : 0.0;  // dropoff processing time
                 unsigned todo = __ballot_sync(VRP_FULL_MASK, valid);
                 __syncwarp();
                 while (todo) {
@@ -312,7 +316,7 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
                     const double rf = __shfl_sync(VRP_FULL_MASK, r, f);
                     const int cf = op_customer(opf);
                     const bool pickf = opf & 1;
-                    const double gene = __shfl_sync(VRP_FULL_MASK, gj, f);
+                    const double pf = __shfl_sync(VRP_FULL_MASK, pj, f);
                     double comp = 0.0;
                     bool fv = false;
                     if (vlane) {
@@ -329,24 +333,33 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
                             comp = arr;
                         }
                     }
-                    const int hint = hint_vehicle(m, gene);
+                    const int hint = __shfl_sync(VRP_FULL_MASK, hj, f);
                     const unsigned fmask = __ballot_sync(VRP_FULL_MASK, fv);
                     int vstar;
                     if (hint >= 0 && hint < 32 && ((fmask >> hint) & 1u)) {
                         vstar = hint;
+                    } else if (INTD) {
+                        // integral completions (< 2^53, exact): one u64 key
+                        // (comp, |v - hint|, v), min over the m vehicle lanes
+                        const int dh = lane > hint ? lane - hint : hint - lane;
+                        uint64_t key = fv ? ((uint64_t)comp << 10) | ((uint64_t)dh << 5) | (uint64_t)lane : ~0ull;
+                        for (int o = mhalf; o; o >>= 1) {
+                            const uint64_t ok = __shfl_xor_sync(VRP_FULL_MASK, key, o);
+                            key = ok < key ? ok : key;
+                        }
+                        vstar = __shfl_sync(VRP_FULL_MASK, (int)(key & 31u), 0);
                     } else {
                         double kc = fv ? comp : DBL_MAX;
                         int kd = fv ? (lane > hint ? lane - hint : hint - lane) : INT_MAX;
                         int kv = fv ? lane : INT_MAX;
-#pragma unroll
-                        for (int o = 16; o; o >>= 1) {
+                        for (int o = mhalf; o; o >>= 1) {
                             double oc = __shfl_xor_sync(VRP_FULL_MASK, kc, o);
                             int od = __shfl_xor_sync(VRP_FULL_MASK, kd, o);
                             int ov = __shfl_xor_sync(VRP_FULL_MASK, kv, o);
                             bool better = oc < kc || (oc == kc && (od < kd || (od == kd && ov < kv)));
                             if (better) { kc = oc; kd = od; kv = ov; }
                         }
-                        vstar = kv;
+                        vstar = __shfl_sync(VRP_FULL_MASK, kv, 0);
                     }
                     const double cstar = __shfl_sync(VRP_FULL_MASK, comp, vstar);
                     if (lane == vstar) {
@@ -358,7 +371,7 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
                     }
                     if (lane == 0) {
                         if (!pickf) {
-                            const double rv = cstar + __ldg(I.p + cf);
+                            const double rv = cstar + pf;
                             if (NARROW) {
                                 ovf |= !(rv < 4294967295.0);
                                 s_ready[cf] = (RT)(ovf ? 0.0 : rv);
