@@ -297,10 +297,12 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
                 // the op's hint vehicle, computed with the window (off the placement chain)
                 const int hj = valid ? hint_vehicle(m, __ldg(g + two_n + op)) : 0;
                 const double pj = valid && !pk ? __ldg(I.p + c) : 0.0;  // dropoff processing time
+                // the pickup's ready time, read once per window; a dropoff placed
+                // inside the window updates its pickup's copy in registers
+                RT rr = pk ? s_ready[c] : (RT)0;
                 unsigned todo = __ballot_sync(VRP_FULL_MASK, valid);
                 __syncwarp();
                 while (todo) {
-                    const RT rr = pk ? s_ready[c] : (RT)0;
                     const bool dropped = NARROW ? rr != (RT)NOT_DROPPED32 : (double)rr >= 0.0;
                     const double r = (double)rr;
                     const bool feas = pk ? (dropped && any_pick && (relax || pick_maxT >= r)) : any_drop;
@@ -369,18 +371,19 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
                         else { int need = 1 - net; lo = need > lo ? need : lo; --net; }
                         ++cnt;
                     }
-                    if (lane == 0) {
-                        if (!pickf) {
-                            const double rv = cstar + pf;
-                            if (NARROW) {
-                                ovf |= !(rv < 4294967295.0);
-                                s_ready[cf] = (RT)(ovf ? 0.0 : rv);
-                            } else {
-                                s_ready[cf] = (RT)rv;
-                            }
+                    if (!pickf) {
+                        const double rv = cstar + pf;
+                        RT rs;
+                        if (NARROW) {
+                            ovf |= !(rv < 4294967295.0);  // warp-uniform
+                            rs = (RT)(ovf ? 0.0 : rv);
+                        } else {
+                            rs = (RT)rv;
                         }
-                        if (seq_scratch) seq[nseq] = (uint32_t)opf | ((uint32_t)vstar << 16);
+                        if (lane == 0) s_ready[cf] = rs;
+                        if (op == opf + 1) rr = rs;  // this window holds the pickup
                     }
+                    if (lane == 0 && seq_scratch) seq[nseq] = (uint32_t)opf | ((uint32_t)vstar << 16);
                     ++nseq;
                     progressed = true;
                     fleet_flags(vlane, t, net, lo, hi, k, relax, any_drop, any_pick, pick_maxT);
