@@ -239,7 +239,7 @@ bucket_sort_kernel(const double *__restrict__ genes, int64_t gstride, int64_t N,
 }
 
 template <bool INTD, typename OutT, bool NARROW = false>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 4)
 decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, int64_t N,
               int relax, double penalty, double *__restrict__ fitness_out,
               double *__restrict__ makespan_out, int32_t *__restrict__ scheduled_out,
