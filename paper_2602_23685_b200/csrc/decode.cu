@@ -21,6 +21,7 @@
 //  emit    (op, vehicle) events are compacted vehicle-major with ballots.
 #include <float.h>
 #include <limits.h>
+#include <stdlib.h>
 
 #include <type_traits>
 
@@ -72,7 +73,9 @@ __device__ __forceinline__ int hint_vehicle(int m, double g) {
     double x = __dmul_rn((double)m, g);
     long long h = (long long)x;
     if (__dsub_rn(x, (double)h) > 1.0 - 1e-9) h += 1;
-    return (int)(h < m ? h : m - 1);
+    // any negative hint orders vehicles like -1 does (|v - h| = v - h) and is
+    // never feasible, so it is clamped to -1 (keeps |v - h| < 64 for the keys)
+    return h < 0 ? -1 : (int)(h < m ? h : m - 1);
 }
 
 __device__ __forceinline__ void bitonic_sort(uint64_t *key, uint16_t *idx, int P2, int lane) {
@@ -344,7 +347,7 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
                         // integral completions (< 2^53, exact): one u64 key
                         // (comp, |v - hint|, v), min over the m vehicle lanes
                         const int dh = lane > hint ? lane - hint : hint - lane;
-                        uint64_t key = fv ? ((uint64_t)comp << 10) | ((uint64_t)dh << 5) | (uint64_t)lane : ~0ull;
+                        uint64_t key = fv ? ((uint64_t)comp << 11) | ((uint64_t)dh << 5) | (uint64_t)lane : ~0ull;
                         for (int o = mhalf; o; o >>= 1) {
                             const uint64_t ok = __shfl_xor_sync(VRP_FULL_MASK, key, o);
                             key = ok < key ? ok : key;
@@ -435,6 +438,320 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Segmented decode: G = 32 / P chromosomes per warp, P = pow2 >= m lanes each
+// (lane sl < m of a segment = vehicle sl).  Every segment runs the same
+// algorithm as decode_kernel on its own P-op window, in lockstep: one step =
+// classify the window, defer the unschedulable prefix, place the first
+// schedulable op.  The per-step ballots, shuffles and the argmin butterfly
+// (log2 P levels) serve G chromosomes at once.  Hint vehicles are staged in
+// shared memory (u8 per gene) with the pending list and the ready table, so a
+// window refill reads shared memory only.
+struct MultiLayout {
+    size_t pend, ready, hint, total;
+};
+
+__host__ __device__ inline MultiLayout multi_layout(int n, int ready_bytes) {
+    MultiLayout L;
+    L.pend = 0;
+    L.ready = align16(2 * (size_t)(2 * n));
+    L.hint = L.ready + align16((size_t)ready_bytes * (size_t)(n + 1));
+    L.total = L.hint + align16((size_t)(2 * n));
+    return L;
+}
+
+template <int P>
+__device__ __forceinline__ double seg_max(double x) {
+#pragma unroll
+    for (int o = P / 2; o; o >>= 1) {
+        double y = __shfl_xor_sync(VRP_FULL_MASK, x, o);
+        x = y > x ? y : x;
+    }
+    return x;
+}
+
+template <int P>
+__device__ __forceinline__ void seg_flags(bool vlane, double t, int net, int lo, int hi, int k, int relax,
+                                          unsigned smask, bool &any_drop, bool &any_pick, double &pick_maxT) {
+    int need = 1 - net, room = k - 1 - net;
+    bool cd = vlane && ((need > lo ? need : lo) <= hi);
+    bool cp = vlane && (lo <= (room < hi ? room : hi));
+    any_drop = (__ballot_sync(VRP_FULL_MASK, cd) & smask) != 0u;
+    any_pick = (__ballot_sync(VRP_FULL_MASK, cp) & smask) != 0u;
+    pick_maxT = relax ? 0.0 : seg_max<P>(cp ? t : -DBL_MAX);
+}
+
+template <bool INTD, typename OutT, bool NARROW, int P>
+__global__ void __launch_bounds__(256, 4)
+decode_multi_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, int64_t N,
+                    int relax, double penalty, double *__restrict__ fitness_out,
+                    double *__restrict__ makespan_out, int32_t *__restrict__ scheduled_out,
+                    int64_t *__restrict__ visits_out, OutT *__restrict__ ops_out, int64_t ostride,
+                    int32_t *__restrict__ lens_out, const uint16_t *__restrict__ order,
+                    uint32_t *__restrict__ seq_scratch, uint8_t *__restrict__ retry,
+                    const uint8_t *__restrict__ only) {
+    using RT = typename std::conditional<NARROW, uint32_t, double>::type;
+    constexpr int G = 32 / P;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    const int seg = lane / P, sl = lane % P, sbase = seg * P;
+    const unsigned smask = (P == 32) ? 0xffffffffu : (((1u << P) - 1u) << sbase);
+    const int n = I.n, m = I.m, k = I.k, two_n = 2 * n;
+    const MultiLayout Ly = multi_layout(n, (int)sizeof(RT));
+    unsigned char *base = smem + ((size_t)warp * G + seg) * Ly.total;
+    volatile RT *s_ready = reinterpret_cast<volatile RT *>(base + Ly.ready);
+    uint16_t *s_pend = reinterpret_cast<uint16_t *>(base + Ly.pend);
+    int8_t *s_hint = reinterpret_cast<int8_t *>(base + Ly.hint);
+    const bool vlane = sl < m;
+    const unsigned lt = lanemask_lt();
+    int mhalf = 1;  // argmin butterfly over segment lanes [0, 2*mhalf) ⊇ the m vehicles
+    while (2 * mhalf < m) mhalf <<= 1;
+    if (m == 1) mhalf = 0;
+
+    for (int64_t c0 = ((int64_t)blockIdx.x * wpb + warp) * G; c0 < N; c0 += (int64_t)gridDim.x * wpb * G) {
+        const int64_t chrom = c0 + seg;
+        const bool real = chrom < N && !(only && !only[chrom]);
+        const int64_t cx = real ? chrom : c0;
+        const double *g = genes + cx * gstride;
+        uint32_t *seq = seq_scratch ? seq_scratch + cx * (int64_t)two_n : nullptr;
+        if (real) {
+            const uint16_t *ord = order + cx * (int64_t)two_n;
+            for (int i = sl; i < two_n; i += P) {
+                s_pend[i] = __ldg(ord + i);
+                s_hint[i] = (int8_t)hint_vehicle(m, __ldg(g + two_n + i));
+            }
+            for (int c = sl; c <= n; c += P) s_ready[c] = NARROW ? (RT)NOT_DROPPED32 : (RT)-1.0;
+        }
+        __syncwarp();
+
+        double t = 0.0;
+        int loc = 0, net = 0, lo = 0, hi = k, cnt = 0;
+        bool any_drop, any_pick;
+        double pick_maxT;
+        seg_flags<P>(vlane, t, net, lo, hi, k, relax, smask, any_drop, any_pick, pick_maxT);
+
+        // segment-uniform progress state
+        int npend = two_n, nw = 0, wbase = -P, pass = 0, nseq = 0;
+        int64_t visits = two_n;
+        bool progressed = false, ovf = false, done = !real || two_n == 0;
+        unsigned todo = 0u;
+        // this lane's op of its segment's window
+        int op = 0, c = 0, hj = 0;
+        bool pk = false;
+        double pj = 0.0;
+        RT rr = (RT)0;
+        while (!__all_sync(VRP_FULL_MASK, done)) {
+            __syncwarp();
+            // ---- refill exhausted windows (a pass ends when its list is exhausted)
+            bool refill = !done && todo == 0u;
+            if (__any_sync(VRP_FULL_MASK, refill)) {
+                if (refill) {
+                    wbase += P;
+                    if (wbase >= npend) {
+                        npend = nw;
+                        ++pass;
+                        if (!progressed || npend == 0 || pass >= two_n) {
+                            done = true;
+                        } else {
+                            visits += npend;
+                            nw = 0;
+                            wbase = 0;
+                            progressed = false;
+                        }
+                    }
+                }
+                refill = refill && !done;
+                const int j = wbase + sl;
+                const bool valid = refill && j < npend;
+                if (refill) {
+                    op = valid ? s_pend[j] : 0;
+                    c = op_customer(op);
+                    pk = op & 1;
+                    hj = valid ? s_hint[op] : 0;
+                    pj = valid && !pk ? __ldg(I.p + c) : 0.0;
+                    rr = pk ? s_ready[c] : (RT)0;
+                }
+                const unsigned vb = __ballot_sync(VRP_FULL_MASK, valid);
+                if (refill) todo = vb & smask;
+            }
+            // ---- classify, defer the unschedulable prefix (in visit order)
+            const bool dropped = NARROW ? rr != (RT)NOT_DROPPED32 : (double)rr >= 0.0;
+            const double r = (double)rr;
+            const bool feas = pk ? (dropped && any_pick && (relax || pick_maxT >= r)) : any_drop;
+            const unsigned fm = __ballot_sync(VRP_FULL_MASK, feas) & todo;
+            const unsigned defm = fm ? (todo & ((1u << (__ffs(fm) - 1)) - 1u)) : todo;
+            if ((defm >> lane) & 1u) s_pend[nw + __popc(defm & lt)] = (uint16_t)op;
+            nw += __popc(defm);
+            const bool place = fm != 0u;
+            const int f = place ? __ffs(fm) - 1 : sbase;
+            todo = place ? (todo & ~((2u << f) - 1u)) : 0u;
+            // ---- place op f (brkga.py:148-193) in every segment that has one
+            const int opf = __shfl_sync(VRP_FULL_MASK, op, f);
+            const double rf = __shfl_sync(VRP_FULL_MASK, r, f);
+            const double pf = __shfl_sync(VRP_FULL_MASK, pj, f);
+            const int hint = __shfl_sync(VRP_FULL_MASK, hj, f);
+            const int cf = op_customer(opf);
+            const bool pickf = opf & 1;
+            double comp = 0.0;
+            bool fv = false;
+            if (vlane && place) {
+                const double leg = dist<INTD>(I, loc, cf);
+                const double arr = t + leg;
+                if (pickf) {
+                    int room = k - 1 - net;
+                    bool cp = lo <= (room < hi ? room : hi);
+                    fv = cp && (relax || t >= rf);
+                    comp = relax ? (arr >= rf ? arr : rf) : arr;
+                } else {
+                    int need = 1 - net;
+                    fv = (need > lo ? need : lo) <= hi;
+                    comp = arr;
+                }
+            }
+            const unsigned fmask = (__ballot_sync(VRP_FULL_MASK, fv) & smask) >> sbase;
+            const bool hintok = hint >= 0 && ((fmask >> hint) & 1u);
+            int vstar = hint;
+            if (__any_sync(VRP_FULL_MASK, place && !hintok)) {
+                int am;
+                if (INTD) {
+                    // integral completions (< 2^53, exact): one u64 key (comp, |v - hint|, v)
+                    const int dh = sl > hint ? sl - hint : hint - sl;
+                    uint64_t key = fv ? ((uint64_t)comp << 11) | ((uint64_t)dh << 5) | (uint64_t)sl : ~0ull;
+                    for (int o = mhalf; o; o >>= 1) {
+                        const uint64_t ok = __shfl_xor_sync(VRP_FULL_MASK, key, o);
+                        key = ok < key ? ok : key;
+                    }
+                    am = (int)(key & 31u);
+                } else {
+                    double kc = fv ? comp : DBL_MAX;
+                    int kd = fv ? (sl > hint ? sl - hint : hint - sl) : INT_MAX;
+                    int kv = fv ? sl : INT_MAX;
+                    for (int o = mhalf; o; o >>= 1) {
+                        double oc = __shfl_xor_sync(VRP_FULL_MASK, kc, o);
+                        int od = __shfl_xor_sync(VRP_FULL_MASK, kd, o);
+                        int ov = __shfl_xor_sync(VRP_FULL_MASK, kv, o);
+                        bool better = oc < kc || (oc == kc && (od < kd || (od == kd && ov < kv)));
+                        if (better) { kc = oc; kd = od; kv = ov; }
+                    }
+                    am = kv;
+                }
+                am = __shfl_sync(VRP_FULL_MASK, am, sbase);
+                if (!hintok) vstar = am;
+            }
+            const double cstar = __shfl_sync(VRP_FULL_MASK, comp, sbase + (vstar & (P - 1)));
+            if (place) {
+                if (sl == vstar) {
+                    t = cstar;
+                    loc = cf;
+                    if (pickf) { int room = k - 1 - net; hi = room < hi ? room : hi; ++net; }
+                    else { int need = 1 - net; lo = need > lo ? need : lo; --net; }
+                    ++cnt;
+                }
+                if (!pickf) {
+                    const double rv = cstar + pf;
+                    RT rs;
+                    if (NARROW) {
+                        ovf |= !(rv < 4294967295.0);  // segment-uniform
+                        rs = (RT)(ovf ? 0.0 : rv);
+                    } else {
+                        rs = (RT)rv;
+                    }
+                    if (sl == 0) s_ready[cf] = rs;
+                    if (op == opf + 1) rr = rs;  // the window holds the pickup
+                }
+                if (sl == 0 && seq) seq[nseq] = (uint32_t)opf | ((uint32_t)vstar << 16);
+                ++nseq;
+                progressed = true;
+            }
+            seg_flags<P>(vlane, t, net, lo, hi, k, relax, smask, any_drop, any_pick, pick_maxT);
+        }
+
+        // ---- fitness (brkga.py:198-200): unused vehicles return at 0 + d[0][0]
+        double ret = vlane ? t + dist<INTD>(I, loc, 0) : -DBL_MAX;
+        const double z = seg_max<P>(ret);
+        if (real && sl == 0) {
+            if (NARROW) retry[chrom] = ovf ? 1 : 0;
+            fitness_out[chrom] = z + penalty * (double)npend;
+            if (makespan_out) makespan_out[chrom] = z;
+            if (scheduled_out) scheduled_out[chrom] = two_n - npend;
+            if (visits_out) visits_out[chrom] = visits;
+        }
+        // ---- emit every chromosome's solution vehicle-major, one at a time
+        if (ops_out) {
+            int off = cnt;
+#pragma unroll
+            for (int o = 1; o < P; o <<= 1) {
+                int y = __shfl_up_sync(VRP_FULL_MASK, off, o, P);
+                if (sl >= o) off += y;
+            }
+            off -= cnt;  // exclusive start of route sl of this segment's chromosome
+            __syncwarp();
+            for (int gi = 0; gi < G; ++gi) {
+                const int64_t ch = c0 + gi;
+                if (ch >= N || (only && !only[ch])) continue;  // warp-uniform
+                const int ns = __shfl_sync(VRP_FULL_MASK, nseq, gi * P);
+                const uint32_t *sq = seq_scratch + ch * (int64_t)two_n;
+                OutT *row = ops_out + ch * ostride;
+                for (int sb = 0; sb < ns; sb += 32) {
+                    const int j = sb + lane;
+                    const bool valid = j < ns;
+                    const uint32_t e = valid ? sq[j] : 0u;
+                    const int o2 = (int)(e & 0xffffu);
+                    const int v = valid ? (int)(e >> 16) : -1;
+                    for (int u = 0; u < m; ++u) {
+                        const unsigned mk = __ballot_sync(VRP_FULL_MASK, v == u);
+                        const int ou = __shfl_sync(VRP_FULL_MASK, off, gi * P + u);
+                        if (v == u) row[ou + __popc(mk & lt)] = (OutT)o2;
+                        if (lane == gi * P + u) off += __popc(mk);
+                    }
+                }
+                for (int j = ns + lane; j < two_n; j += 32) row[j] = (OutT)-1;
+            }
+            if (real && lens_out && vlane) lens_out[chrom * m + sl] = cnt;
+        }
+        __syncwarp();
+    }
+}
+
+template <bool INTD, typename OutT, bool NARROW, int P>
+int launch_m(const DevInstance &I, const double *genes, int64_t gstride, int64_t N, int relax,
+             double penalty, double *fitness, double *makespan, int32_t *scheduled, int64_t *visits,
+             void *ops_out, int64_t ostride, int32_t *lens_out, const uint16_t *order, uint32_t *seq,
+             uint8_t *retry, const uint8_t *only, cudaStream_t stream, int sm_count) {
+    constexpr int G = 32 / P;
+    auto kern = decode_multi_kernel<INTD, OutT, NARROW, P>;
+    const size_t per_warp = multi_layout(I.n, NARROW ? 4 : 8).total * G;
+    static size_t cached_pw = 0;
+    static int cached_w = 0, cached_blocks = 0;
+    if (cached_pw != per_warp) {
+        int best_w = 0, best_res = 0, best_blocks = 0;
+        for (int w = 8; w >= 1; --w) {
+            size_t bytes = per_warp * (size_t)w;
+            if (bytes > 227 * 1024) continue;
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+                return -1;
+            int blocks = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32 * w, bytes) != cudaSuccess)
+                return -1;
+            if (blocks * w > best_res) { best_res = blocks * w; best_w = w; best_blocks = blocks; }
+        }
+        if (!best_res) return -2;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per_warp * best_w));
+        cached_pw = per_warp; cached_w = best_w; cached_blocks = best_blocks;
+    }
+    const size_t bytes = per_warp * (size_t)cached_w;
+    const int64_t nwarps = (N + G - 1) / G;
+    int64_t want = (nwarps + cached_w - 1) / cached_w;
+    int64_t grid = (int64_t)cached_blocks * sm_count;
+    if (grid > want) grid = want;
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, 32 * cached_w, bytes, stream>>>(I, genes, gstride, N, relax, penalty, fitness,
+                                                         makespan, scheduled, visits,
+                                                         static_cast<OutT *>(ops_out), ostride, lens_out,
+                                                         order, seq, retry, only);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
 // one decode_kernel launch, occupancy planned once per (instantiation, n)
 template <bool INTD, typename OutT, bool NARROW>
 int launch_k(const DevInstance &I, const double *genes, int64_t gstride, int64_t N, int relax,
@@ -473,6 +790,35 @@ int launch_k(const DevInstance &I, const double *genes, int64_t gstride, int64_t
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
 }
 
+// segmented kernel for m <= 16 (G = 32 / P chromosomes per warp), the
+// warp-per-chromosome kernel above that, or when VRP_DECODE_SINGLE is set
+template <bool INTD, typename OutT, bool NARROW>
+int launch_any(const DevInstance &I, const double *genes, int64_t gstride, int64_t N, int relax,
+               double penalty, double *fitness, double *makespan, int32_t *scheduled, int64_t *visits,
+               void *ops_out, int64_t ostride, int32_t *lens_out, const uint16_t *order, uint32_t *seq,
+               uint8_t *retry, const uint8_t *only, cudaStream_t stream, int sm_count) {
+    const char *single = getenv("VRP_DECODE_SINGLE");
+    // below n = 500 (a280: 2.8 KB of shared memory per chromosome); at n = 999
+    // (10 KB) residency drops to ~20 chromosomes per SM and the warp-per-
+    // chromosome kernel is 2.8x faster (measured)
+    const bool seg = !(single && single[0] && single[0] != '0') && I.n < 500;
+    if (seg && I.m <= 4)
+        return launch_m<INTD, OutT, NARROW, 4>(I, genes, gstride, N, relax, penalty, fitness, makespan, scheduled,
+                                               visits, ops_out, ostride, lens_out, order, seq, retry, only,
+                                               stream, sm_count);
+    if (seg && I.m <= 8)
+        return launch_m<INTD, OutT, NARROW, 8>(I, genes, gstride, N, relax, penalty, fitness, makespan, scheduled,
+                                               visits, ops_out, ostride, lens_out, order, seq, retry, only,
+                                               stream, sm_count);
+    if (seg && I.m <= 16)
+        return launch_m<INTD, OutT, NARROW, 16>(I, genes, gstride, N, relax, penalty, fitness, makespan,
+                                                scheduled, visits, ops_out, ostride, lens_out, order, seq, retry,
+                                                only, stream, sm_count);
+    return launch_k<INTD, OutT, NARROW>(I, genes, gstride, N, relax, penalty, fitness, makespan, scheduled,
+                                        visits, ops_out, ostride, lens_out, order, seq, retry, only, stream,
+                                        sm_count);
+}
+
 template <bool INTD, typename OutT>
 int launch_t(const DevInstance &I, const double *genes, int64_t gstride, int64_t N, int relax,
              double penalty, double *fitness, double *makespan, int32_t *scheduled, int64_t *visits,
@@ -485,9 +831,10 @@ int launch_t(const DevInstance &I, const double *genes, int64_t gstride, int64_t
     uint8_t *retry = nullptr;
     if (cudaMallocAsync(&order, sizeof(uint16_t) * (size_t)N * two_n, stream) != cudaSuccess) return -1;
     if (ops_out && cudaMallocAsync(&seq, sizeof(uint32_t) * (size_t)N * two_n, stream) != cudaSuccess) return -1;
-    // narrow tables only where shared memory limits residency (measured: below
-    // n ~ 500 the uint32 conversions cost more than the extra warps give)
-    const bool narrow = INTD && I.n >= 500;
+    // narrow tables where shared memory limits residency (measured: a280
+    // +25 % with the segmented kernel; below n ~ 200 registers bound it)
+    const char *nm = getenv("VRP_DECODE_NARROW_MIN");  // (ablation knob)
+    const bool narrow = INTD && I.n >= (nm ? atoi(nm) : 200);
     if (narrow && cudaMallocAsync(&retry, (size_t)N, stream) != cudaSuccess) return -1;
     uint8_t *fb = nullptr;
     if (cudaMallocAsync(&fb, (size_t)N, stream) != cudaSuccess) return -1;
@@ -519,15 +866,15 @@ int launch_t(const DevInstance &I, const double *genes, int64_t gstride, int64_t
     }
     int rc;
     if (narrow) {  // narrow pass, then the wide kernel over the (normally no) flagged chromosomes
-        rc = launch_k<INTD, OutT, true>(I, genes, gstride, N, relax, penalty, fitness, makespan, scheduled,
+        rc = launch_any<INTD, OutT, true>(I, genes, gstride, N, relax, penalty, fitness, makespan, scheduled,
                                         visits, ops_out, ostride, lens_out, order, seq, retry, nullptr, stream,
                                         sm_count);
         if (!rc)
-            rc = launch_k<INTD, OutT, false>(I, genes, gstride, N, relax, penalty, fitness, makespan,
+            rc = launch_any<INTD, OutT, false>(I, genes, gstride, N, relax, penalty, fitness, makespan,
                                              scheduled, visits, ops_out, ostride, lens_out, order, seq,
                                              nullptr, retry, stream, sm_count);
     } else {
-        rc = launch_k<INTD, OutT, false>(I, genes, gstride, N, relax, penalty, fitness, makespan, scheduled,
+        rc = launch_any<INTD, OutT, false>(I, genes, gstride, N, relax, penalty, fitness, makespan, scheduled,
                                          visits, ops_out, ostride, lens_out, order, seq, nullptr, nullptr,
                                          stream, sm_count);
     }

@@ -200,3 +200,42 @@ def test_decode_sort_paths_clustered_priorities(key):
     np.testing.assert_array_equal(r["ops"].cpu().numpy(), ref["ops"])
     np.testing.assert_array_equal(r["fitness"].cpu().numpy(), ref["fitness"])
     np.testing.assert_array_equal(r["visits"].cpu().numpy(), ref["visits"])
+
+
+def test_decode_narrow_overflow_segmented_kernel():
+    """200 <= n < 500 decodes through the segmented K3 kernel (several
+    chromosomes per warp) with the narrow ready table: a scaled a280 instance
+    pushes about half the chromosomes past 2^32 -- the wide fix-up pass (also
+    segmented) must reproduce the oracle for those, the narrow pass for the
+    rest."""
+    from paper_2602_23685_b200.instance import Instance
+    base = config_instance("a280")
+    d, p = base.arrays()
+    genes = I.chromosomes(base.n, 96, (23, 23))
+    z0 = O.decode_batch(base, genes[:16])["makespan"]
+    scale = float(np.floor(2.0**32 / np.median(z0)))
+    assert d.max() * scale < 2.0**31 and p.max() * scale < 2.0**31
+    inst = Instance.from_arrays(d * scale, p * scale, base.m, base.k, label="a280-scaled")
+    ref = O.decode_batch(inst, genes)
+    assert (ref["makespan"] > 2.0**32).any() and (ref["makespan"] < 2.0**32).any()
+    for op_dtype in (torch.int16, torch.int32):
+        r = dev().decode_batch(inst, _cuda(genes), op_dtype=op_dtype)
+        np.testing.assert_array_equal(r["ops"].cpu().numpy().astype(np.int32), ref["ops"])
+        np.testing.assert_array_equal(r["lens"].cpu().numpy(), ref["lens"])
+        np.testing.assert_array_equal(r["fitness"].cpu().numpy(), ref["fitness"])
+        np.testing.assert_array_equal(r["visits"].cpu().numpy(), ref["visits"])
+
+
+@pytest.mark.parametrize("key", CONFIG_KEYS)
+def test_decode_warp_per_chromosome_kernel(key, golden, monkeypatch):
+    """VRP_DECODE_SINGLE=1 forces the warp-per-chromosome K3 kernel (used at
+    n >= 500 and m > 16) on every config: same goldens, relaxed and strict."""
+    monkeypatch.setenv("VRP_DECODE_SINGLE", "1")
+    inst = config_instance(key)
+    pre = f"{key}/"
+    genes = I.chromosomes(inst.n, golden[pre + "dec_ops"].shape[0], (136, CID[key]))
+    for tag, g, relax in (("dec", genes, True), ("strict", genes[: golden[pre + "enc_genes"].shape[0]], False)):
+        r = dev().decode_batch(inst, _cuda(g), relax=relax)
+        np.testing.assert_array_equal(r["ops"].cpu().numpy(), golden[pre + f"{tag}_ops"])
+        for f in ("fitness", "visits"):
+            np.testing.assert_array_equal(r[f].cpu().numpy(), golden[pre + f"{tag}_{f}"], err_msg=f)
