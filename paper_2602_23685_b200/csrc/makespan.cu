@@ -172,7 +172,11 @@ struct RouteStream {
 // residency is set by registers, not shared memory.  A candidate that runs
 // out of slots is capacity-infeasible (status CAPACITY regardless) -- or,
 // should that reasoning ever fail, goes to the 64-bit fix-up pass (ST_RETRY).
-template <typename OpT, bool INTD, int MODE, bool REC, bool NARROW, bool COMPACT = false>
+//
+// MC > 0 fixes the fleet size at compile time (MC == I.m; the m = 6 fleets of
+// every benchmark config beyond gr17): lane/candidate indexing, the slot
+// classes and the rotation OR then cost no run-time tests.
+template <typename OpT, bool INTD, int MODE, bool REC, bool NARROW, bool COMPACT = false, int MC = 0>
 __global__ void __launch_bounds__(256)
 makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 const int32_t *__restrict__ lens, int64_t N, int G, double *__restrict__ z_out,
@@ -183,7 +187,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
-    const int n = I.n, m = I.m, k = I.k, two_n = 2 * n;
+    const int n = I.n, m = MC ? MC : I.m, k = I.k, two_n = 2 * n;
     // NARROW: event times in uint32 (every value the narrow table can hold);
     // a wrap-around is detected and sends the candidate to the 64-bit pass
     using TT = typename std::conditional<NARROW, uint32_t, TimeT<INTD>>::type;
@@ -480,12 +484,12 @@ int plan(Kern kern, int n, int m, int mode, int ready_bytes, bool compact, Shape
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)out.smem) == cudaSuccess ? 0 : -1;
 }
 
-template <typename OpT, bool INTD, int MODE, bool REC, bool NARROW, bool COMPACT = false>
+template <typename OpT, bool INTD, int MODE, bool REC, bool NARROW, bool COMPACT = false, int MC = 0>
 int launch_t(const DevInstance &I, const void *ops, int64_t stride, const int32_t *lens,
              int64_t N, double *z, int32_t *status, double *returns, int32_t *bottleneck,
              double *arrival, double *timev, int32_t *q0, cudaStream_t stream, int sm_count,
              int fixup) {
-    auto kern = makespan_kernel<OpT, INTD, MODE, REC, NARROW, COMPACT>;
+    auto kern = makespan_kernel<OpT, INTD, MODE, REC, NARROW, COMPACT, MC>;
     static int cached_n = -1, cached_m = -1;
     static Shape sh;
     if (cached_n != I.n || cached_m != I.m) {
@@ -513,7 +517,10 @@ int launch_narrow(const DevInstance &I, const void *ops, int64_t stride, const i
                   int64_t N, double *z, int32_t *status, double *returns, int32_t *bottleneck,
                   cudaStream_t stream, int sm_count) {
     int rc;
-    if (MODE != MODE_TWO && I.m * I.k <= SLOTS)  // slot table (see makespan_kernel: COMPACT)
+    if (MODE != MODE_TWO && I.m == 6 && I.k <= SLOTS / 6)  // slot table, m fixed at 6
+        rc = launch_t<OpT, true, MODE, false, true, true, 6>(I, ops, stride, lens, N, z, status, returns, bottleneck,
+                                                             nullptr, nullptr, nullptr, stream, sm_count, 0);
+    else if (MODE != MODE_TWO && I.m * I.k <= SLOTS)  // slot table (see makespan_kernel: COMPACT)
         rc = launch_t<OpT, true, MODE, false, true, true>(I, ops, stride, lens, N, z, status, returns, bottleneck,
                                                           nullptr, nullptr, nullptr, stream, sm_count, 0);
     else
