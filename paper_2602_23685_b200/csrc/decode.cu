@@ -241,7 +241,9 @@ bucket_sort_kernel(const double *__restrict__ genes, int64_t gstride, int64_t N,
     (void)lt;
 }
 
-template <bool INTD, typename OutT, bool NARROW = false>
+// MC > 0 fixes the fleet size at compile time (MC == I.m): the argmin
+// butterfly, the hint product and the vehicle-major emit loop are unrolled.
+template <bool INTD, typename OutT, bool NARROW = false, int MC = 0>
 __global__ void __launch_bounds__(256, 4)
 decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, int64_t N,
               int relax, double penalty, double *__restrict__ fitness_out,
@@ -255,7 +257,7 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
-    const int n = I.n, m = I.m, k = I.k, two_n = 2 * n;
+    const int n = I.n, m = MC ? MC : I.m, k = I.k, two_n = 2 * n;
     const DecodeLayout Ly = decode_layout(n, (int)sizeof(RT));
     unsigned char *base = smem + (size_t)warp * Ly.total;
     volatile RT *s_ready = reinterpret_cast<volatile RT *>(base + Ly.ready);
@@ -753,12 +755,12 @@ int launch_m(const DevInstance &I, const double *genes, int64_t gstride, int64_t
 }
 
 // one decode_kernel launch, occupancy planned once per (instantiation, n)
-template <bool INTD, typename OutT, bool NARROW>
+template <bool INTD, typename OutT, bool NARROW, int MC = 0>
 int launch_k(const DevInstance &I, const double *genes, int64_t gstride, int64_t N, int relax,
              double penalty, double *fitness, double *makespan, int32_t *scheduled, int64_t *visits,
              void *ops_out, int64_t ostride, int32_t *lens_out, const uint16_t *order, uint32_t *seq,
              uint8_t *retry, const uint8_t *only, cudaStream_t stream, int sm_count) {
-    auto kern = decode_kernel<INTD, OutT, NARROW>;
+    auto kern = decode_kernel<INTD, OutT, NARROW, MC>;
     const size_t per_warp = decode_layout(I.n, NARROW ? 4 : 8).total;
     static size_t cached_pw = 0;
     static int cached_w = 0, cached_blocks = 0;
@@ -814,6 +816,10 @@ int launch_any(const DevInstance &I, const double *genes, int64_t gstride, int64
         return launch_m<INTD, OutT, NARROW, 16>(I, genes, gstride, N, relax, penalty, fitness, makespan,
                                                 scheduled, visits, ops_out, ostride, lens_out, order, seq, retry,
                                                 only, stream, sm_count);
+    if (I.m == 6)  // the fleet of every benchmark config beyond gr17
+        return launch_k<INTD, OutT, NARROW, 6>(I, genes, gstride, N, relax, penalty, fitness, makespan, scheduled,
+                                               visits, ops_out, ostride, lens_out, order, seq, retry, only, stream,
+                                               sm_count);
     return launch_k<INTD, OutT, NARROW>(I, genes, gstride, N, relax, penalty, fitness, makespan, scheduled,
                                         visits, ops_out, ostride, lens_out, order, seq, retry, only, stream,
                                         sm_count);
