@@ -23,8 +23,9 @@ __device__ __forceinline__ bool op_is_pick(int op) { return op & 1; }
 // identical double value with half the L2 sector footprint per row.
 template <bool INTD>
 __device__ __forceinline__ double dist(const DevInstance &I, int a, int b) {
-    if (INTD) return (double)__ldg(I.d32 + (int64_t)a * I.W + b);
-    return __ldg(I.d + (int64_t)a * I.W + b);
+    const uint32_t idx = (uint32_t)a * (uint32_t)I.W + (uint32_t)b;  // n <= 16383: W^2 < 2^28
+    if (INTD) return (double)__ldg(I.d32 + idx);
+    return __ldg(I.d + idx);
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
