@@ -483,7 +483,7 @@ __device__ __forceinline__ void seg_flags(bool vlane, double t, int net, int lo,
     pick_maxT = relax ? 0.0 : seg_max<P>(cp ? t : -DBL_MAX);
 }
 
-template <bool INTD, typename OutT, bool NARROW, int P>
+template <bool INTD, typename OutT, bool NARROW, int P, int MC = 0>  // MC: as decode_kernel
 __global__ void __launch_bounds__(256, 4)
 decode_multi_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, int64_t N,
                     int relax, double penalty, double *__restrict__ fitness_out,
@@ -498,7 +498,7 @@ decode_multi_kernel(DevInstance I, const double *__restrict__ genes, int64_t gst
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     const int seg = lane / P, sl = lane % P, sbase = seg * P;
     const unsigned smask = (P == 32) ? 0xffffffffu : (((1u << P) - 1u) << sbase);
-    const int n = I.n, m = I.m, k = I.k, two_n = 2 * n;
+    const int n = I.n, m = MC ? MC : I.m, k = I.k, two_n = 2 * n;
     const MultiLayout Ly = multi_layout(n, (int)sizeof(RT));
     unsigned char *base = smem + ((size_t)warp * G + seg) * Ly.total;
     volatile RT *s_ready = reinterpret_cast<volatile RT *>(base + Ly.ready);
@@ -715,13 +715,13 @@ decode_multi_kernel(DevInstance I, const double *__restrict__ genes, int64_t gst
     }
 }
 
-template <bool INTD, typename OutT, bool NARROW, int P>
+template <bool INTD, typename OutT, bool NARROW, int P, int MC = 0>
 int launch_m(const DevInstance &I, const double *genes, int64_t gstride, int64_t N, int relax,
              double penalty, double *fitness, double *makespan, int32_t *scheduled, int64_t *visits,
              void *ops_out, int64_t ostride, int32_t *lens_out, const uint16_t *order, uint32_t *seq,
              uint8_t *retry, const uint8_t *only, cudaStream_t stream, int sm_count) {
     constexpr int G = 32 / P;
-    auto kern = decode_multi_kernel<INTD, OutT, NARROW, P>;
+    auto kern = decode_multi_kernel<INTD, OutT, NARROW, P, MC>;
     const size_t per_warp = multi_layout(I.n, NARROW ? 4 : 8).total * G;
     static size_t cached_pw = 0;
     static int cached_w = 0, cached_blocks = 0;
@@ -804,6 +804,10 @@ int launch_any(const DevInstance &I, const double *genes, int64_t gstride, int64
     // (10 KB) residency drops to ~20 chromosomes per SM and the warp-per-
     // chromosome kernel is 2.8x faster (measured)
     const bool seg = !(single && single[0] && single[0] != '0') && I.n < 500;
+    if (seg && I.m == 6)  // the fleet of every benchmark config beyond gr17
+        return launch_m<INTD, OutT, NARROW, 8, 6>(I, genes, gstride, N, relax, penalty, fitness, makespan,
+                                                  scheduled, visits, ops_out, ostride, lens_out, order, seq, retry,
+                                                  only, stream, sm_count);
     if (seg && I.m <= 4)
         return launch_m<INTD, OutT, NARROW, 4>(I, genes, gstride, N, relax, penalty, fitness, makespan, scheduled,
                                                visits, ops_out, ostride, lens_out, order, seq, retry, only,
