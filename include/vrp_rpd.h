@@ -165,6 +165,20 @@ int vrp_destroy_batch(vrp_instance_t h, const int32_t *ops, int64_t op_stride, c
                       int32_t *out_ops, int64_t out_stride, int32_t *out_lens, int32_t *removed,
                       int64_t removed_stride, int32_t *nremoved, int64_t N, void *stream);
 
+/* insertion.remove_customers (insertion.py:379-397) alone, on N solutions:
+ * both ops of the picked customers (picked[N][picked_stride], npicked[N]) are
+ * removed and the capacity cascade runs; outputs as vrp_destroy_batch. */
+int vrp_remove_batch(vrp_instance_t h, const int32_t *ops, int64_t op_stride, const int32_t *lens,
+                     const int32_t *picked, int64_t picked_stride, const int32_t *npicked,
+                     int32_t *out_ops, int64_t out_stride, int32_t *out_lens, int32_t *removed,
+                     int64_t removed_stride, int32_t *nremoved, int64_t N, void *stream);
+
+/* insertion.removal_gains (insertion.py:538-569): the makespan reduction of
+ * removing each customer under fixed ready times, gains[N][gains_stride]
+ * (index c = 1..n; index 0 = 0) for N complete solutions (DEVICE). */
+int vrp_removal_gains(vrp_instance_t h, const int32_t *ops, int64_t op_stride, const int32_t *lens,
+                      double *gains, int64_t gains_stride, int64_t N, void *stream);
+
 /* Local-search neighbourhoods (alns.py:416-487 pickup_repositioning /
  * cross_agent_relocation; baselines.py:372-455 two_opt_improve) materialised
  * as a candidate batch for
@@ -189,6 +203,12 @@ int vrp_ls_build(vrp_instance_t h, int32_t kind, const int32_t *base_ops, const 
                  const int32_t *entries, const int64_t *entry_start, int64_t n_entries,
                  const int64_t *index_list, int64_t first, int64_t count, void *out_ops,
                  int32_t op_bytes, int32_t *out_lens, void *stream);
+
+/* The simulated-annealing acceptance threshold exp(x) of alns.py:588
+ * (`rng.random() < math.exp(-delta / T)`) as vrp_alns_iterate computes it:
+ * fp64 exp rounded correctly (double-double evaluation, csrc/ddexp.cuh).
+ * x, y: n DEVICE doubles. */
+int vrp_sa_exp(const double *x, double *y, int64_t n, void *stream);
 
 /* One ALNS worker (alns.py:536-640 run_alns locals), DEVICE-resident.
  * weights/scores/attempts are indexed in the reference's operator order:

@@ -155,83 +155,37 @@ def shaw_relatedness(instance, schedule, ci: int, cj: int) -> float:
 
 
 # --------------------------------------------------------------------------
-# destroy (host)
+# destroy (device: K6)
 # --------------------------------------------------------------------------
-
-def _power_law_pick(items, rng, power: float = WORST_POWER):
-    idx = int(rng.random() ** power * len(items))
-    return items[min(idx, len(items) - 1)]
-
-
-def _sample(items, size: int, rng) -> list:
-    pool = list(items)
-    n = len(pool)
-    for i in range(size):
-        j = i + int(rng.integers(n - i))
-        pool[i], pool[j] = pool[j], pool[i]
-    return pool[:size]
-
 
 def destroy(instance, solution: Solution, operator: str, q: int, rng):
     """Remove (at least) q customers with one of the six operators
-    (alns.py:182-251); returns (partial Solution, removed list)."""
+    (alns.py:182-251), then the capacity cascade of remove_customers
+    (insertion.py:379-397); returns (partial Solution, removed list).
+
+    Runs K6 (``vrp_destroy_batch``) on one solution.  ``rng`` must be a
+    ``Generator(Philox)`` for draw-for-draw parity: its state goes to the
+    device and comes back advanced exactly as the reference's operator
+    advances it.  Any other generator is replaced by a Philox stream keyed
+    from it (rng.as_philox)."""
+    from . import device as Dev
+    import torch
     n = instance.n
     if n == 0 or all(not t for t in solution.tours):
         raise EmptySolution("nothing to remove")
-    q = min(q, n)
-    customers = list(instance.customers)
-    q_min = min(removal_bounds(n)[0], n)
-    d = instance.d
-    if operator == "random":
-        picked = _sample(customers, q, rng)
-    elif operator == "worst":
-        gains = insertion.removal_gains(instance, solution)
-        ranked = sorted(customers, key=lambda c: (-gains[c], c))
-        picked = []
-        while len(picked) < q:
-            c = _power_law_pick(ranked, rng)
-            ranked.remove(c)
-            picked.append(c)
-    elif operator == "shaw":
-        sched = evaluate(instance, solution)
-        seed_c = customers[int(rng.integers(n))]
-        picked = [seed_c]
-        pool = [c for c in customers if c != seed_c]
-        while len(picked) < q and pool:
-            ref = picked[int(rng.integers(len(picked)))]
-            best = min(pool, key=lambda c: (shaw_relatedness(instance, sched, ref, c), c))
-            pool.remove(best)
-            picked.append(best)
-    elif operator == "cluster":
-        center = customers[int(rng.integers(n))]
-        ranked = sorted((c for c in customers if c != center), key=lambda c: (d[center][c], c))
-        picked = [center] + ranked[:q - 1]
-    elif operator == "route":
-        non_empty = [v for v, t in enumerate(solution.tours) if t]
-        v = non_empty[int(rng.integers(len(non_empty)))]
-        picked = sorted({c for c, _ in solution.tours[v]})
-        if len(picked) < q_min:
-            pool = [c for c in customers if c not in picked]
-            while len(picked) < q_min and pool:
-                best = min(pool, key=lambda c: (min(d[c][x] for x in picked), c))
-                pool.remove(best)
-                picked.append(best)
-    elif operator == "critical_path":
-        sched = evaluate(instance, solution)
-        v = sched.bottleneck()
-        on_route = sorted({c for c, _ in solution.tours[v]})
-        if len(on_route) >= q:
-            picked = _sample(on_route, q, rng)
-        else:
-            picked = list(on_route)
-            if len(picked) < q_min:
-                gains = insertion.removal_gains(instance, solution)
-                pool = sorted((c for c in customers if c not in picked), key=lambda c: (-gains[c], c))
-                picked.extend(pool[:q_min - len(picked)])
-    else:
+    if operator not in DESTROY_OPERATORS:
         raise ValueError(f"unknown destroy operator {operator!r}")
-    tours, removed = insertion.remove_customers(instance, solution, picked)
-    return Solution.from_lists(tours), removed
+    gen = R.as_philox(rng)
+    ops, lens = solution.to_arrays(n)
+    state = R.state_to_device(gen)[None]
+    r = Dev.destroy_batch(instance, ops[None, :2 * n], lens[None],
+                          torch.tensor([Dev.DESTROY_CODES[operator]], dtype=torch.int32),
+                          torch.tensor([min(int(q), n)], dtype=torch.int32),
+                          min(removal_bounds(n)[0], n), state)
+    R.state_from_device(gen, state[0])
+    nr = int(r["nremoved"][0].item())
+    partial = Solution.from_arrays(r["ops"][0].cpu().numpy(), r["lens"][0].cpu().numpy())
+    return partial, [int(c) for c in r["removed"][0, :nr].cpu().numpy()]
 
 
 # --------------------------------------------------------------------------
@@ -264,38 +218,51 @@ def repair(instance, partial: Solution, removed, operator: str, rng) -> Solution
 # --------------------------------------------------------------------------
 
 def sweep_order(instance) -> list:
-    d = instance.d
-    cs = list(instance.customers)
-    a = max(cs, key=lambda c: (d[0][c], -c))
-    b = max(cs, key=lambda c: (d[a][c], -c))
-    return sorted(cs, key=lambda c: (d[a][c] - d[b][c], d[0][c], c))
+    """Customers in the reference's coordinate-free sweep order
+    (alns.py:290-298): anchor a = the customer farthest from the depot, b =
+    the customer farthest from a (lowest index on ties), then ascending
+    (d[a][c] - d[b][c], d[0][c], c)."""
+    D = np.asarray(instance.arrays()[0] if hasattr(instance, "arrays") else instance.d, np.float64)
+    cs = np.arange(1, instance.n + 1)
+    a = 1 + int(np.argmax(D[0, 1:]))  # argmax keeps the first maximum: the lowest customer
+    b = 1 + int(np.argmax(D[a, 1:]))
+    order = np.lexsort((cs, D[0, cs], D[a, cs] - D[b, cs]))
+    return [int(c) for c in cs[order]]
 
 
 def _balance_sectors(instance, sectors) -> list:
-    w = {c: 2.0 * instance.d[0][c] + instance.p[c] for c in instance.customers}
-    sectors = [list(s) for s in sectors]
-    loads = [sum(w[c] for c in s) for s in sectors]
-    mean = sum(loads) / len(loads) if loads else 0.0
+    """Rebalance sector workloads w(c) = 2 d[0][c] + p[c] (alns.py:301-327):
+    while some load deviates from the mean by >= 10 %, move the customer of
+    the heaviest sector whose move to the lightest lowers the peak load most
+    (first such customer in sector order); stop after 2n moves or when no move
+    lowers the peak.  Loads are summed with the builtin sum, as there."""
+    D = np.asarray(instance.arrays()[0] if hasattr(instance, "arrays") else instance.d, np.float64)
+    P = np.asarray(instance.arrays()[1] if hasattr(instance, "arrays") else instance.p, np.float64)
+    w = 2.0 * D[0] + P  # w[c] for c = 1..n (w[0] unused)
+    secs = [list(x) for x in sectors]
+    loads = [sum(float(w[c]) for c in x) for x in secs]
+    if not loads:
+        return secs
+    mean = sum(loads) / len(loads)
     for _ in range(2 * instance.n):
         if mean <= 0 or max(abs(x - mean) for x in loads) < 0.10 * mean:
             break
-        hi = max(range(len(loads)), key=lambda i: loads[i])
-        lo = min(range(len(loads)), key=lambda i: loads[i])
-        if not sectors[hi]:
+        arr = np.asarray(loads)
+        hi, lo = int(np.argmax(arr)), int(np.argmin(arr))
+        if not secs[hi]:
             break
-        best_c, best_peak = None, max(loads)
-        for c in sectors[hi]:
-            peak = max(loads[hi] - w[c], loads[lo] + w[c],
-                       *(loads[i] for i in range(len(loads)) if i not in (hi, lo)))
-            if peak < best_peak:
-                best_c, best_peak = c, peak
-        if best_c is None:
+        others = np.delete(arr, [hi, lo])
+        rest = others.max() if others.size else -np.inf
+        wc = w[np.asarray(secs[hi])]
+        peaks = np.maximum(np.maximum(arr[hi] - wc, arr[lo] + wc), rest)
+        j = int(np.argmin(peaks))
+        if not peaks[j] < arr.max():
             break
-        sectors[hi].remove(best_c)
-        sectors[lo].append(best_c)
-        loads[hi] -= w[best_c]
-        loads[lo] += w[best_c]
-    return sectors
+        c = secs[hi].pop(j)
+        secs[lo].append(c)
+        loads[hi] -= float(w[c])
+        loads[lo] += float(w[c])
+    return secs
 
 
 def _route_sector(instance, customers) -> list:
@@ -495,29 +462,30 @@ def worker_seed(seed: int, worker: int) -> int:
 
 
 class _PoolShare:
-    """Best incumbent shared inside a pool (lockstep pool: no locks needed)."""
+    """A pool's shared incumbent (alns.py:503-533 semantics).  Workers of a
+    pool advance in lockstep on one host thread, so no lock is needed.
+    ``offer`` keeps strictly better solutions (remembering the source
+    worker), ``poll`` returns the incumbent to every other worker, and
+    ``merge`` moves a strictly better incumbent across two shares (the
+    receiver forgets the source)."""
 
     def __init__(self):
-        self.best_z = math.inf
-        self.best_sol = None
-        self.src = None
+        self.best_z, self.best_sol, self.src = math.inf, None, None
 
     def offer(self, worker: int, z: float, sol: Solution) -> None:
         if z < self.best_z:
             self.best_z, self.best_sol, self.src = z, sol, worker
 
     def poll(self, worker: int):
-        if self.best_sol is not None and self.src != worker:
-            return self.best_z, self.best_sol
-        return None
+        if self.best_sol is None or self.src == worker:
+            return None
+        return self.best_z, self.best_sol
 
     def merge(self, other: "_PoolShare") -> None:
-        mine = (self.best_z, self.best_sol, self.src)
-        theirs = (other.best_z, other.best_sol, other.src)
-        if mine[0] < theirs[0]:
-            other.best_z, other.best_sol, other.src = mine[0], mine[1], None
-        if theirs[0] < mine[0] and theirs[0] < self.best_z:
-            self.best_z, self.best_sol, self.src = theirs[0], theirs[1], None
+        if self.best_z < other.best_z:
+            other.best_z, other.best_sol, other.src = self.best_z, self.best_sol, None
+        elif other.best_z < self.best_z:
+            self.best_z, self.best_sol, self.src = other.best_z, other.best_sol, None
 
 
 class _Worker:

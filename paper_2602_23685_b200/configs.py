@@ -9,8 +9,8 @@ acceptance seed, ``pkg/tests/test_acceptance.py:35``).  Coordinates are
 integer draws from ``numpy.random.default_rng(coord_seed)``, recorded in the
 TSPLIB COMMENT line.
 
-gr17 is loaded from ``tests/golden/gr17_base.json``, the reference's own
-parse of ``pkg/data/gr17.tsp`` written by ``tests/golden/make_golden.py``.
+gr17 is loaded from ``data/gr17_base.json`` (package data), the reference's own
+parse of ``pkg/data/gr17.tsp`` as written by ``tests/golden/make_golden.py``.
 """
 from __future__ import annotations
 
@@ -23,7 +23,7 @@ from .instance import Instance, VariantSpec, build_instance, parse_tsplib
 
 VARIANT_SEED = 136
 REPO = Path(__file__).resolve().parent.parent
-GR17_JSON = REPO / "tests" / "golden" / "gr17_base.json"
+GR17_JSON = Path(__file__).resolve().parent / "data" / "gr17_base.json"
 
 
 @dataclass(frozen=True)

@@ -20,16 +20,17 @@
 //
 // Scratch per worker: the K5 repair layout + the destroy layout below.
 // fp64 in the reference's order (-fmad=false).  Two documented last-ulp
-// caveats: the power-6 pick uses a double-double x^6 rounded once (glibc's pow
-// is correctly rounded in all but pathological cases) and the SA test uses
-// CUDA's exp (<= 1 ulp); a disagreement needs a uniform draw to land inside
-// that ulp (p ~ 2^-52 per iteration).
+// caveats: the power-6 pick uses a double-double x^6 rounded once, and the SA
+// test uses a correctly rounded exp (ddexp.cuh) where the host uses glibc's,
+// which misrounds ~0.07 % of inputs; a disagreement needs such an input AND a
+// uniform draw inside that one ulp (p < 2^-63 per test).
 #include <float.h>
 #include <math.h>
 
 #include "common.cuh"
 #include "kernels.h"
 #include "repair_core.cuh"
+#include "ddexp.cuh"
 
 namespace {
 
@@ -225,6 +226,8 @@ __device__ void removal_gains(const DevInstance &I, const int *cur, const int *l
     const int n = I.n, m = I.m;
     const int L = lane < m ? lens[lane] : 0;
     const int *row = cur + (lane < m ? D.off[lane] : 0);
+    for (int c = lane; c <= n; c += 32) D.posd[c] = D.posp[c] = -1;  // absent from a partial solution
+    __syncwarp();
     {
         double t = 0.0;
         int loc = 0;
@@ -265,7 +268,7 @@ __device__ void removal_gains(const DevInstance &I, const int *cur, const int *l
         if (D.ret[v] > cur_mk) cur_mk = D.ret[v];
     for (int c = lane + 1; c <= n; c += 32) {
         const int pd = D.posd[c], pk = D.posp[c];
-        const int vd = pd >> 16, vp = pk >> 16;
+        const int vd = pd >= 0 ? pd >> 16 : -1, vp = pk >= 0 ? pk >> 16 : -1;
         bool have = false;
         double nm = 0.0;
         for (int v = 0; v < m; ++v) {
@@ -275,6 +278,7 @@ __device__ void removal_gains(const DevInstance &I, const int *cur, const int *l
         for (int a = 0; a < 2; ++a) {
             const int v = a ? vp : vd;
             if (a && vp == vd) break;
+            if (v < 0) continue;
             const int *rv = cur + D.off[v];
             const int Lv = lens[v];
             int i0, i1, cnt;
@@ -695,7 +699,7 @@ alns_kernel(DevInstance I, vrp_alns_params P, vrp_alns_worker *__restrict__ work
                     }
                     S.n_trace += 1;
                 }
-            } else if (S.temperature > 0 && gen.next_double() < exp(-(zc - S.z) / S.temperature)) {
+            } else if (S.temperature > 0 && gen.next_double() < ddexp::exp_cr(-(zc - S.z) / S.temperature)) {
                 acc = 1;
                 S.z = zc;
                 S.scores[dop] += P.sigma3;
@@ -752,7 +756,8 @@ destroy_kernel(DevInstance I, const int32_t *__restrict__ ops, int64_t stride, c
                const int32_t *__restrict__ opcode, const int32_t *__restrict__ qv, int32_t q_min,
                vrp_philox *__restrict__ states, int32_t *__restrict__ out_ops, int64_t ostride,
                int32_t *__restrict__ out_lens, int32_t *__restrict__ removed, int64_t rstride,
-               int32_t *__restrict__ nremoved, unsigned char *__restrict__ scratch, size_t per, int64_t N) {
+               int32_t *__restrict__ nremoved, unsigned char *__restrict__ scratch, size_t per, int64_t N,
+               const int32_t *__restrict__ picked, int64_t pstride, const int32_t *__restrict__ npicked) {
     __shared__ int s_len[MAXM];
     const int lane = threadIdx.x;
     const int64_t w = blockIdx.x;
@@ -770,10 +775,21 @@ destroy_kernel(DevInstance I, const int32_t *__restrict__ ops, int64_t stride, c
         __syncwarp();
     }
     PhiloxGen gen;
-    if (lane == 0) gen.s = states[w];
-    int q = qv[w];
-    if (q > n) q = n;
-    destroy<INTD>(I, opcode[w], q, q_min < n ? q_min : n, cur, clen, D, C, lane, gen);
+    if (picked) {  // remove_customers alone: the caller's customers (insertion.py:379-397)
+        for (int c = lane; c <= n; c += 32) D.flag[c] = 0;
+        __syncwarp();
+        const int np = npicked[w];
+        for (int i = lane; i < np; i += 32) {
+            const int c = picked[w * pstride + i];
+            if (c >= 1 && c <= n) D.flag[c] = 1;
+        }
+        __syncwarp();
+    } else {
+        if (lane == 0) gen.s = states[w];
+        int q = qv[w];
+        if (q > n) q = n;
+        destroy<INTD>(I, opcode[w], q, q_min < n ? q_min : n, cur, clen, D, C, lane, gen);
+    }
     remove_flagged(X, cur, clen, D);
     int32_t *oo = out_ops + w * ostride;
     store_rows(X, oo, out_lens + w * m);
@@ -783,8 +799,32 @@ destroy_kernel(DevInstance I, const int32_t *__restrict__ ops, int64_t stride, c
     const int nr = compact_marked(D.flag, removed + w * rstride, n, lane);
     if (lane == 0) {
         nremoved[w] = nr;
-        states[w] = gen.s;
+        if (!picked) states[w] = gen.s;
     }
+}
+
+// insertion.removal_gains (insertion.py:538-569) alone: gains[w][c], c = 1..n
+// (gains[w][0] = 0)
+template <bool INTD>
+__global__ void __launch_bounds__(32)
+gains_kernel(DevInstance I, const int32_t *__restrict__ ops, int64_t stride, const int32_t *__restrict__ lens,
+             double *__restrict__ gains, int64_t gstride, unsigned char *__restrict__ scratch, size_t per,
+             int64_t N) {
+    const int lane = threadIdx.x;
+    const int64_t w = blockIdx.x;
+    if (w >= N) return;
+    const int n = I.n, m = I.m, C = 2 * n + 2;
+    Dx D = bind_dx(scratch + (size_t)w * per, n, m);
+    const int32_t *cur = ops + w * stride, *clen = lens + w * m;
+    {
+        const int L = lane < m ? clen[lane] : 0;
+        const int o = lane_offset(L, lane);
+        if (lane < m) D.off[lane] = o;
+        __syncwarp();
+    }
+    removal_gains<INTD>(I, cur, clen, D, C, lane);
+    double *g = gains + w * gstride;
+    for (int c = lane; c <= n; c += 32) g[c] = c ? D.gains[c] : 0.0;
 }
 
 }  // namespace
@@ -814,7 +854,8 @@ int launch_alns(const DevInstance &I, const vrp_alns_params &P, vrp_alns_worker 
 int launch_destroy(const DevInstance &I, const int32_t *ops, int64_t stride, const int32_t *lens,
                    const int32_t *opcode, const int32_t *q, int32_t q_min, vrp_philox *states,
                    int32_t *out_ops, int64_t ostride, int32_t *out_lens, int32_t *removed,
-                   int64_t rstride, int32_t *nremoved, int64_t N, cudaStream_t stream) {
+                   int64_t rstride, int32_t *nremoved, int64_t N, cudaStream_t stream,
+                   const int32_t *picked, int64_t pstride, const int32_t *npicked) {
     if (N <= 0) return 0;
     const size_t per = al8(alns_scratch_bytes(I.n, I.m));
     unsigned char *scratch = nullptr;
@@ -822,12 +863,43 @@ int launch_destroy(const DevInstance &I, const int32_t *ops, int64_t stride, con
     if (I.integral)
         destroy_kernel<true><<<(unsigned)N, 32, 0, stream>>>(I, ops, stride, lens, opcode, q, q_min, states,
                                                              out_ops, ostride, out_lens, removed, rstride,
-                                                             nremoved, scratch, per, N);
+                                                             nremoved, scratch, per, N, picked, pstride,
+                                                             npicked);
     else
         destroy_kernel<false><<<(unsigned)N, 32, 0, stream>>>(I, ops, stride, lens, opcode, q, q_min, states,
                                                               out_ops, ostride, out_lens, removed, rstride,
-                                                              nremoved, scratch, per, N);
+                                                              nremoved, scratch, per, N, picked, pstride,
+                                                              npicked);
     const cudaError_t e = cudaPeekAtLastError();
     cudaFreeAsync(scratch, stream);
     return e == cudaSuccess ? 0 : -1;
+}
+
+namespace {
+__global__ void sa_exp_kernel(const double *__restrict__ x, double *__restrict__ y, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = ddexp::exp_cr(x[i]);
+}
+}  // namespace
+
+int launch_gains(const DevInstance &I, const int32_t *ops, int64_t stride, const int32_t *lens, double *gains,
+                 int64_t gstride, int64_t N, cudaStream_t stream) {
+    if (N <= 0) return 0;
+    const size_t per = al8(make_dlayout(I.n, I.m).total);
+    unsigned char *scratch = nullptr;
+    if (cudaMallocAsync(&scratch, per * (size_t)N, stream) != cudaSuccess) return -1;
+    if (I.integral)
+        gains_kernel<true><<<(unsigned)N, 32, 0, stream>>>(I, ops, stride, lens, gains, gstride, scratch, per, N);
+    else
+        gains_kernel<false><<<(unsigned)N, 32, 0, stream>>>(I, ops, stride, lens, gains, gstride, scratch, per, N);
+    const cudaError_t e = cudaPeekAtLastError();
+    cudaFreeAsync(scratch, stream);
+    return e == cudaSuccess ? 0 : -1;
+}
+
+int launch_sa_exp(const double *x, double *y, int64_t n, cudaStream_t stream) {
+    if (n <= 0) return 0;
+    const int64_t blocks = (n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096;
+    sa_exp_kernel<<<(unsigned)blocks, 256, 0, stream>>>(x, y, n);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
 }

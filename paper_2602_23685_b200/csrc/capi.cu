@@ -257,6 +257,43 @@ int vrp_destroy_batch(vrp_instance_t h, const int32_t *ops, int64_t op_stride, c
                          "vrp_destroy_batch");
 }
 
+int vrp_remove_batch(vrp_instance_t h, const int32_t *ops, int64_t op_stride, const int32_t *lens,
+                     const int32_t *picked, int64_t picked_stride, const int32_t *npicked, int32_t *out_ops,
+                     int64_t out_stride, int32_t *out_lens, int32_t *removed, int64_t removed_stride,
+                     int32_t *nremoved, int64_t N, void *stream) {
+    if (!h) return fail(VRP_EINVAL, "null instance%s");
+    if (N < 0) return fail(VRP_EINVAL, "vrp_remove_batch: N < 0%s");
+    if (N == 0) return 0;
+    if (!ops || !lens || !picked || !npicked || !out_ops || !out_lens || !removed || !nremoved)
+        return fail(VRP_EINVAL, "vrp_remove_batch: null buffer%s");
+    const int64_t n = h->dev.n;
+    if (op_stride < 2 * n || out_stride < 2 * n || removed_stride < n || picked_stride < 0)
+        return fail(VRP_EINVAL, "vrp_remove_batch: stride too small%s");
+    return launch_result(launch_destroy(h->dev, ops, op_stride, lens, nullptr, nullptr, 0, nullptr, out_ops,
+                                        out_stride, out_lens, removed, removed_stride, nremoved, N,
+                                        static_cast<cudaStream_t>(stream), picked, picked_stride, npicked),
+                         "vrp_remove_batch");
+}
+
+int vrp_removal_gains(vrp_instance_t h, const int32_t *ops, int64_t op_stride, const int32_t *lens,
+                      double *gains, int64_t gains_stride, int64_t N, void *stream) {
+    if (!h) return fail(VRP_EINVAL, "null instance%s");
+    if (N < 0) return fail(VRP_EINVAL, "vrp_removal_gains: N < 0%s");
+    if (N == 0) return 0;
+    if (!ops || !lens || !gains) return fail(VRP_EINVAL, "vrp_removal_gains: null buffer%s");
+    if (op_stride < 2 * (int64_t)h->dev.n || gains_stride < (int64_t)h->dev.n + 1)
+        return fail(VRP_EINVAL, "vrp_removal_gains: stride too small%s");
+    return launch_result(launch_gains(h->dev, ops, op_stride, lens, gains, gains_stride, N,
+                                      static_cast<cudaStream_t>(stream)),
+                         "vrp_removal_gains");
+}
+
+int vrp_sa_exp(const double *x, double *y, int64_t n, void *stream) {
+    if (n < 0) return fail(VRP_EINVAL, "vrp_sa_exp: n < 0%s");
+    if (n && (!x || !y)) return fail(VRP_EINVAL, "vrp_sa_exp: null buffer%s");
+    return launch_result(launch_sa_exp(x, y, n, static_cast<cudaStream_t>(stream)), "vrp_sa_exp");
+}
+
 int vrp_ls_build(vrp_instance_t h, int32_t kind, const int32_t *base_ops, const int32_t *base_lens,
                  const int32_t *entries, const int64_t *entry_start, int64_t n_entries,
                  const int64_t *index_list, int64_t first, int64_t count, void *out_ops,

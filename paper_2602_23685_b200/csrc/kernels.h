@@ -46,7 +46,12 @@ int launch_alns(const DevInstance &I, const vrp_alns_params &P, vrp_alns_worker 
 int launch_destroy(const DevInstance &I, const int32_t *ops, int64_t stride, const int32_t *lens,
                    const int32_t *opcode, const int32_t *q, int32_t q_min, vrp_philox *states,
                    int32_t *out_ops, int64_t ostride, int32_t *out_lens, int32_t *removed,
-                   int64_t rstride, int32_t *nremoved, int64_t N, cudaStream_t stream);
+                   int64_t rstride, int32_t *nremoved, int64_t N, cudaStream_t stream,
+                   const int32_t *picked = nullptr, int64_t pstride = 0, const int32_t *npicked = nullptr);
+int launch_gains(const DevInstance &I, const int32_t *ops, int64_t stride, const int32_t *lens, double *gains,
+                 int64_t gstride, int64_t N, cudaStream_t stream);
+
+int launch_sa_exp(const double *x, double *y, int64_t n, cudaStream_t stream);
 
 // ls.cu (batched local-search candidate builder)
 int launch_ls_build(int kind, int n, int m, const int32_t *base_ops, const int32_t *base_lens,

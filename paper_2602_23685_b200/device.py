@@ -295,6 +295,53 @@ def destroy_batch(instance, ops, lens, operators, q, q_min, states, stream=None)
     return out
 
 
+def remove_batch(instance, ops, lens, picked, npicked, stream=None):
+    """insertion.remove_customers on N solutions (vrp_remove_batch, K6's
+    removal + capacity cascade).  ops [N, >=2n] / lens [N, m] int32, picked
+    [N, P] int32 customers with npicked [N] valid per row.  Returns dict(ops
+    [N, 2n] partials, lens [N, m], removed [N, n] sorted, nremoved [N])."""
+    di = device_instance(instance)
+    o = _cuda(ops, torch.int32)
+    ln = _cuda(lens, torch.int32)
+    pk = _cuda(picked, torch.int32)
+    npk = _cuda(npicked, torch.int32)
+    if o.dim() == 1:
+        o, ln = o.unsqueeze(0), ln.unsqueeze(0)
+    if pk.dim() == 1:
+        pk = pk.unsqueeze(0)
+    Nn = o.shape[0]
+    if ln.shape != (Nn, di.m) or pk.shape[0] != Nn or npk.shape != (Nn,):
+        raise ValueError("remove_batch: ops/lens/picked/npicked shapes disagree")
+    dev = o.device
+    out = {"ops": torch.empty((Nn, 2 * di.n), dtype=torch.int32, device=dev),
+           "lens": torch.empty((Nn, di.m), dtype=torch.int32, device=dev),
+           "removed": torch.zeros((Nn, di.n), dtype=torch.int32, device=dev),
+           "nremoved": torch.empty(Nn, dtype=torch.int32, device=dev)}
+    N.check(N.lib().vrp_remove_batch(di.handle, N.ptr(o), row_stride(o), N.ptr(ln), N.ptr(pk),
+                                     row_stride(pk), N.ptr(npk), N.ptr(out["ops"]), 2 * di.n,
+                                     N.ptr(out["lens"]), N.ptr(out["removed"]), di.n,
+                                     N.ptr(out["nremoved"]), Nn, N.stream_handle(stream)),
+            "vrp_remove_batch")
+    return out
+
+
+def removal_gains_batch(instance, ops, lens, stream=None):
+    """insertion.removal_gains on N complete solutions (vrp_removal_gains):
+    fp64 [N, n+1] device tensor, column c = gain of customer c (column 0 = 0)."""
+    di = device_instance(instance)
+    o = _cuda(ops, torch.int32)
+    ln = _cuda(lens, torch.int32)
+    if o.dim() == 1:
+        o, ln = o.unsqueeze(0), ln.unsqueeze(0)
+    Nn = o.shape[0]
+    if ln.shape != (Nn, di.m):
+        raise ValueError(f"lens must be [N, m={di.m}]")
+    gains = torch.empty((Nn, di.n + 1), dtype=torch.float64, device=o.device)
+    N.check(N.lib().vrp_removal_gains(di.handle, N.ptr(o), row_stride(o), N.ptr(ln), N.ptr(gains),
+                                      di.n + 1, Nn, N.stream_handle(stream)), "vrp_removal_gains")
+    return gains
+
+
 # vrp_alns_worker / vrp_alns_params (include/vrp_rpd.h), field for field
 ALNS_WORKER_DTYPE = np.dtype([
     ("rng", np.uint8, 96), ("z", "<f8"), ("z_best", "<f8"), ("temperature", "<f8"), ("t_init", "<f8"),

@@ -9,8 +9,8 @@ bit-identical to the reference including its RNG consumption when driven by a
 (the ALNS worker batch); ``reinsert_all`` is the reference's one-instance
 signature on top of it.
 
-``remove_customers`` (:379-397) and ``removal_gains`` (:538-569) are host
-helpers used by the destroy operators (small next to repair).
+``remove_customers`` (:379-397) and ``removal_gains`` (:538-569) run K6's
+device code (``vrp_remove_batch`` / ``vrp_removal_gains``) on one solution.
 """
 from __future__ import annotations
 
@@ -95,72 +95,29 @@ def reinsert_all(ctx: InsertionContext, removed, regret_k: int = 0, rng=None) ->
     ctx.tours = [list(t) for t in Solution.from_arrays(o[0], l[0]).tours]
 
 
-def _first_capacity_break(tours, k):
-    for tour in tours:
-        s, lo, hi = 0, 0, k
-        for c, kind in tour:
-            if kind is _D:
-                lo = max(lo, 1 - s)
-                s -= 1
-            else:
-                hi = min(hi, k - 1 - s)
-                s += 1
-            if lo > hi:
-                return c
-    return None
-
-
 def remove_customers(instance, solution: Solution, customers) -> tuple:
-    """Drop both ops of `customers`, cascading routes left without a feasible
-    initial load (insertion.py:358-397).  Returns (tours, sorted removed)."""
-    gone = set(customers)
-    tours = [[op for op in tour if op[0] not in gone] for tour in solution.tours]
-    while (broken := _first_capacity_break(tours, instance.k)) is not None:
-        gone.add(broken)
-        tours = [[op for op in tour if op[0] != broken] for tour in tours]
-    return tours, sorted(gone)
-
-
-def _walk_return(seq, d, ready) -> float:
-    if not seq:
-        return 0.0
-    t, loc = 0.0, 0
-    for c, kind in seq:
-        t += d[loc][c]
-        loc = c
-        if kind is _P:
-            r = ready.get(c)
-            if r is not None and r > t:
-                t = r
-    return t + d[loc][0]
+    """Drop both operations of ``customers`` and cascade every customer whose
+    removal leaves a route without a feasible initial load
+    (insertion.py:379-397).  Runs K6's removal on the device
+    (vrp_remove_batch, batch of one).  Returns (tours, sorted removed)."""
+    n = instance.n
+    ops, lens = solution.to_arrays(n)
+    picked = np.asarray(sorted({int(c) for c in customers}), np.int32)
+    if picked.size == 0:
+        picked = np.zeros(1, np.int32)
+        count = 0
+    else:
+        count = picked.size
+    r = Dev.remove_batch(instance, ops[None, :2 * n], lens[None], picked[None], np.array([count], np.int32))
+    o, ln = r["ops"][0].cpu().numpy(), r["lens"][0].cpu().numpy()
+    nr = int(r["nremoved"][0].item())
+    removed = [int(c) for c in r["removed"][0, :nr].cpu().numpy()]
+    return [list(t) for t in Solution.from_arrays(o, ln).tours], removed
 
 
 def removal_gains(instance, solution: Solution) -> dict:
-    """Makespan reduction estimate per customer under fixed ready times
-    (insertion.py:538-569)."""
-    d, p = instance.d, instance.p
-    tours = [list(t) for t in solution.tours]
-    ready = {}
-    for tour in tours:
-        t, loc = 0.0, 0
-        for c, kind in tour:
-            t += d[loc][c]
-            loc = c
-            if kind is _D:
-                ready[c] = t + p[c]
-    rets = [_walk_return(tour, d, ready) for tour in tours]
-    where: dict = {}
-    for v, tour in enumerate(tours):
-        for c, _ in tour:
-            where.setdefault(c, set()).add(v)
-    cur = max(rets) if rets else 0.0
-    gains = {}
-    for c in instance.customers:
-        touched = where.get(c, set())
-        new_mk = max((r for v, r in enumerate(rets) if v not in touched), default=0.0)
-        for v in touched:
-            r = _walk_return([op for op in tours[v] if op[0] != c], d, ready)
-            if r > new_mk:
-                new_mk = r
-        gains[c] = cur - new_mk
-    return gains
+    """Estimated makespan reduction of removing each customer, ready times
+    held fixed (insertion.py:538-569), on the device (vrp_removal_gains)."""
+    ops, lens = solution.to_arrays(instance.n)
+    g = Dev.removal_gains_batch(instance, ops[None, :2 * instance.n], lens[None])[0].cpu().numpy()
+    return {c: float(g[c]) for c in instance.customers}

@@ -146,6 +146,16 @@ def _world(group):
     return 0, 1
 
 
+def _host_staged(group) -> bool:
+    """gloo has no CUDA point-to-point path: stage device tensors through the
+    host (the NCCL path sends device memory directly over NVLink)."""
+    return dist.get_backend(group) == "gloo"
+
+
+def _wire(t: torch.Tensor, staged: bool) -> torch.Tensor:
+    return t.cpu() if staged and t.is_cuda else t
+
+
 def migrate(engine: IslandEngine, k: int, group=None) -> None:
     """Ring migration: my k best -> rank+1; rank-1's k best replace my k worst."""
     rank, world = _world(group)
@@ -153,8 +163,9 @@ def migrate(engine: IslandEngine, k: int, group=None) -> None:
         return
     order = engine.order()
     k = min(k, engine.pop.shape[0] // 2)
-    send_genes = engine.pop[order[:k]].contiguous()
-    send_fit = engine.fit[order[:k]].contiguous()
+    staged = _host_staged(group)
+    send_genes = _wire(engine.pop[order[:k]].contiguous(), staged)
+    send_fit = _wire(engine.fit[order[:k]].contiguous(), staged)
     recv_genes = torch.empty_like(send_genes)
     recv_fit = torch.empty_like(send_fit)
     nxt, prv = (rank + 1) % world, (rank - 1) % world
@@ -163,7 +174,8 @@ def migrate(engine: IslandEngine, k: int, group=None) -> None:
     for req in dist.batch_isend_irecv(ops):
         req.wait()
     worst = order[-k:]
-    engine.admit(worst, recv_genes, recv_fit)
+    dev = engine.pop.device
+    engine.admit(worst, recv_genes.to(dev), recv_fit.to(dev))
 
 
 def sync_incumbent(engine: IslandEngine, group=None):
@@ -175,6 +187,9 @@ def sync_incumbent(engine: IslandEngine, group=None):
     genes = engine.best_genes.clone()
     if world < 2:
         return float(best.item()), 0, genes
+    dev = genes.device
+    staged = _host_staged(group)
+    best, genes = _wire(best, staged), _wire(genes, staged)
     gmin = best.clone()
     dist.all_reduce(gmin, op=dist.ReduceOp.MIN, group=group)
     cand = torch.tensor([rank if bool(best.item() == gmin.item()) else world],
@@ -183,7 +198,7 @@ def sync_incumbent(engine: IslandEngine, group=None):
     winner = int(cand.item())
     src = dist.get_global_rank(group, winner) if group is not None else winner
     dist.broadcast(genes, src=src, group=group)
-    return float(gmin.item()), winner, genes
+    return float(gmin.item()), winner, genes.to(dev)
 
 
 def run_islands(instance, params: B.BrkgaParams, island: IslandParams | None = None, seed: int = 0,

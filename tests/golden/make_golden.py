@@ -8,7 +8,7 @@ exist on the GPU box):
 Outputs (committed):
   tests/golden/golden.npz     -- inputs (small) and reference outputs
   tests/golden/golden.json    -- metadata: versions, per-config instance hashes
-  tests/golden/gr17_base.json -- the reference's parse of pkg/data/gr17.tsp
+  paper_2602_23685_b200/data/gr17_base.json -- the reference's parse of pkg/data/gr17.tsp
 
 Reference functions exercised (paths relative to pkg/src/vrp_rpd/):
   instance.parse_tsplib / build_instance   instance.py:200-401
@@ -105,7 +105,7 @@ def main():
         p = np.array(inst.p, dtype=np.float64)
         n, m, k = inst.n, inst.m, inst.k
         if key == "gr17":
-            inst.save(HERE / "gr17_base.json")
+            inst.save(HERE.parent.parent / "paper_2602_23685_b200" / "data" / "gr17_base.json")
         # pin our own instance builder against the reference's
         ours = C.config_instance(key)
         od, op = ours.arrays()

@@ -5,15 +5,10 @@ import numpy as np
 import pytest
 
 from conftest import config_instance
-from test_host_alns import check_destroy
 from paper_2602_23685_b200 import alns as A
 from paper_2602_23685_b200.schedule import Solution
 
 pytestmark = pytest.mark.gpu
-
-
-def test_destroy_with_schedule_matches_reference(golden, golden_meta):
-    check_destroy(golden, golden_meta, ("shaw", "critical_path"))
 
 
 @pytest.mark.parametrize("key", ["gr17", "eil51", "kroA100"])

@@ -8,6 +8,8 @@ import torch
 
 import inputs as I
 from conftest import config_instance
+from oracle import destroy_oracle as DO
+from oracle import oracle as O
 from paper_2602_23685_b200 import alns as A
 from paper_2602_23685_b200 import device as DV
 from paper_2602_23685_b200 import rng as R
@@ -60,7 +62,7 @@ def test_destroy_kernel_matches_reference_goldens(golden, golden_meta):
 @pytest.mark.parametrize("key,count", [("gr17", 48), ("eil51", 48), ("kroA100", 36), ("a280", 18),
                                        ("dsj1000", 6)])
 def test_destroy_kernel_vs_host_at_scale(key, count, golden):
-    """Fresh solutions and seeds; every operator; q across [q_min, q_max]."""
+    """K6 against the destroy oracle: fresh seeds; every operator; q across [q_min, q_max]."""
     inst = config_instance(key)
     n = inst.n
     base = golden[f"{key}/dec_ops"], golden[f"{key}/dec_lens"]
@@ -75,11 +77,11 @@ def test_destroy_kernel_vs_host_at_scale(key, count, golden):
     o, l, rem = _destroy_dev(inst, sols, names, qs, g_dev)
     for i in range(count):
         g = I.philox(71, CID[key], i)
-        partial, removed = A.destroy(inst, sols[i], names[i], qs[i], g)
-        po, pl = partial.to_arrays(n)
+        po, pl, removed = DO.destroy(inst, base[0][i % base[0].shape[0]], base[1][i % base[0].shape[0]],
+                                     names[i], qs[i], g)
         assert rem[i] == removed, (names[i], i)
         np.testing.assert_array_equal(l[i], pl, err_msg=f"{names[i]} {i}")
-        np.testing.assert_array_equal(o[i], po[:2 * n], err_msg=f"{names[i]} {i}")
+        np.testing.assert_array_equal(o[i], po, err_msg=f"{names[i]} {i}")
         assert np.array_equal(R.state_bytes(g), R.state_bytes(g_dev[i])), (names[i], i)
 
 
@@ -110,7 +112,8 @@ def _same_stats(a, b):
     assert a.attempts == b.attempts and a.weight_rows == b.weight_rows
 
 
-@pytest.mark.parametrize("key,iters,seed", [("eil51", 450, 3), ("kroA100", 120, 4), ("a280", 25, 5)])
+@pytest.mark.parametrize("key,iters,seed", [("eil51", 450, 3), ("kroA100", 120, 4), ("a280", 25, 5),
+                                            ("dsj1000", 4, 6)])
 def test_device_engine_equals_host_engine(key, iters, seed):
     """Longer single trajectories (local search at 200/400 included)."""
     inst = config_instance(key)
@@ -154,3 +157,57 @@ def test_device_engine_equals_host_engine_fractional_instance():
     b2, s2 = A.run_alns(inst, params, seed=8, initial=initial, engine="host")
     assert b1 == b2
     _same_stats(s1, s2)
+
+
+def test_sa_exp_correctly_rounded():
+    """The SA threshold exp (alns.py:588) that vrp_alns_iterate uses is the
+    correctly rounded fp64 exp: checked against 50-digit decimal exp."""
+    import decimal
+    from paper_2602_23685_b200 import _native as N
+    decimal.getcontext().prec = 50
+    g = np.random.default_rng(9)
+    x = np.concatenate([-g.random(40000) * 40, g.uniform(-700, 700, 4000), -g.random(2000) * 1e-6,
+                        [0.0, -0.5, -1.0, -707.9, 708.9]])
+    want = np.array([float(decimal.Decimal(float(v)).exp()) for v in x])
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    N.check(N.lib().vrp_sa_exp(N.ptr(xd), N.ptr(yd), x.size, N.stream_handle()), "vrp_sa_exp")
+    np.testing.assert_array_equal(yd.cpu().numpy(), want)
+
+
+def test_reference_signature_destroy_and_removal_api(golden, golden_meta):
+    """The drop-in signatures run K6 on the device: alns.destroy (batch of
+    one, the caller's Philox generator round-tripped) equals the reference's
+    destroy goldens; insertion.remove_customers equals the repair goldens'
+    partials; insertion.removal_gains equals the oracle's."""
+    from paper_2602_23685_b200 import insertion as INS
+    for i, rec in enumerate(golden_meta["destroys"]):
+        inst = config_instance(rec["key"])
+        sol = Solution.from_arrays(golden[f"{rec['key']}/dec_ops"][rec["case"]],
+                                   golden[f"{rec['key']}/dec_lens"][rec["case"]])
+        rng = I.philox(41, CID[rec["key"]], rec["case"])
+        partial, removed = A.destroy(inst, sol, rec["operator"], rec["q"], rng)
+        assert removed == list(golden[f"destroy/{i}/removed"]), rec
+        ops, lens = partial.to_arrays(inst.n)
+        np.testing.assert_array_equal(lens, golden[f"destroy/{i}/lens"])
+        np.testing.assert_array_equal(ops, golden[f"destroy/{i}/ops"])
+        st = rng.bit_generator.state
+        assert [int(x) for x in st["state"]["counter"]] == rec["final_counter"]
+        assert int(st["buffer_pos"]) == rec["final_buffer_pos"]
+        assert int(st["has_uint32"]) == rec["final_has_uint32"]
+    for i, rec in enumerate(golden_meta["repairs"]):
+        inst = config_instance(rec["key"])
+        sol = Solution.from_arrays(golden[f"{rec['key']}/dec_ops"][rec["case"]],
+                                   golden[f"{rec['key']}/dec_lens"][rec["case"]])
+        tours, removed = INS.remove_customers(inst, sol, [int(x) for x in golden[f"repair/{i}/pick"]])
+        assert removed == list(golden[f"repair/{i}/removed"])
+        ops, lens = Solution.from_lists(tours).to_arrays(inst.n)
+        np.testing.assert_array_equal(lens, golden[f"repair/{i}/partial_lens"])
+        np.testing.assert_array_equal(ops, golden[f"repair/{i}/partial_ops"])
+    for key in ("gr17", "eil51", "kroA100", "a280", "dsj1000"):
+        inst = config_instance(key)
+        for j in range(2):
+            o, l = golden[f"{key}/dec_ops"][j], golden[f"{key}/dec_lens"][j]
+            gains = INS.removal_gains(inst, Solution.from_arrays(o, l))
+            want = DO.removal_gains(inst, o, l)
+            assert [gains[c] for c in inst.customers] == list(want[1:]), key

@@ -239,3 +239,26 @@ def test_decode_warp_per_chromosome_kernel(key, golden, monkeypatch):
         np.testing.assert_array_equal(r["ops"].cpu().numpy(), golden[pre + f"{tag}_ops"])
         for f in ("fitness", "visits"):
             np.testing.assert_array_equal(r[f].cpu().numpy(), golden[pre + f"{tag}_{f}"], err_msg=f)
+
+
+@pytest.mark.parametrize("key", CONFIG_KEYS)
+def test_bottleneck_out_vs_oracle(key, golden):
+    """vrp_makespan_batch's bottleneck output = Schedule.bottleneck
+    (schedule.py:105-110: the first vehicle with the largest return, strict >)
+    on decoded, block and swap-perturbed candidates, exact and evaluate modes."""
+    inst = config_instance(key)
+    pre = f"{key}/"
+    fams = [(golden[pre + "dec_ops"], golden[pre + "dec_lens"]),
+            (golden[pre + "blk_ops"], golden[pre + "blk_lens"]),
+            (golden[pre + "swp_ops"], golden[pre + "dec_lens"])]
+    blk = I.block_candidates(inst.n, inst.m, inst.k, 64, (74, CID[key], 0))
+    fams.append(blk)
+    for ops, lens in fams:
+        for mode, name in ((0, "exact"), (1, "evaluate")):
+            r = dev().makespan_batch(inst, _cuda(ops), _cuda(lens), mode=mode, want_returns=True,
+                                     want_bottleneck=True)
+            z, st, ret = O.makespan_batch(inst, ops, lens, mode=name, want_returns=True)
+            ok = st == 0
+            assert np.array_equal(r["status"].cpu().numpy(), st)
+            want = np.argmax(ret, axis=1)  # first maximum (strict >), like Schedule.bottleneck
+            np.testing.assert_array_equal(r["bottleneck"].cpu().numpy()[ok], want[ok], err_msg=name)

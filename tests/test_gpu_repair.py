@@ -120,3 +120,47 @@ def test_repair_non_integral_instance_vs_oracle():
             np.testing.assert_array_equal(l[i], rl)
             np.testing.assert_array_equal(o[i], ro)
         assert same_state(dev_gens[i], g), i
+
+
+def _dsj_cases():
+    """16 repairs at the dsj1000 size (n = 999): block-structured solutions
+    (route-local customers, so the removed set is exactly the q picked) with
+    q in {2, 24, 49}, plus decoded solutions whose capacity cascade grows
+    q = 2 to ~50 removed customers (insertion.py:379-397)."""
+    inst = config_instance("dsj1000")
+    n = inst.n
+    blk_ops, blk_lens = I.block_candidates(n, inst.m, inst.k, 12, (71, 5, 0))
+    dec = O.decode_batch(inst, I.chromosomes(n, 4, (71, 5)))
+    srcs = [(blk_ops[i], blk_lens[i], (2, 24, 49)[i % 3]) for i in range(12)]
+    srcs += [(dec["ops"][i], dec["lens"][i], 2) for i in range(4)]
+    parts, plens, removed, rks = [], [], [], []
+    for i, (ops, lens, q) in enumerate(srcs):
+        pick = I.philox(72, 5, i).choice(np.arange(1, n + 1), size=q, replace=False)
+        o, l, r = O.remove_customers(inst, ops, lens, pick)
+        parts.append(o[:2 * n]); plens.append(l); removed.append(r)
+        rks.append((0, 2, 3, inst.m)[i % 4])
+    return inst, np.stack(parts), np.stack(plens), removed, rks
+
+
+def test_repair_batch_vs_oracle_dsj1000():
+    """K5 at n = 999 (the size the product runs it at, pipeline.py) against
+    the oracle's reinsert_all: tours, RepairFailed and generator state;
+    12 cases with a Generator(Philox) and 4 deterministic (rng=None)."""
+    inst, parts, plens, removed, rks = _dsj_cases()
+    assert sorted({len(r) for r in removed[:12]}) == [2, 24, 49]
+    assert min(len(r) for r in removed[12:]) > 2  # the cascade fired
+    with_rng = list(range(12))
+    without = list(range(12, 16))
+    for group, use in ((with_rng, True), (without, False)):
+        gens = [I.philox(73, 5, i) for i in group] if use else None
+        o, l, st = INS.reinsert_batch(inst, parts[group], plens[group], [removed[i] for i in group],
+                                      [rks[i] for i in group], gens)
+        for j, i in enumerate(group):
+            g = I.philox(73, 5, i) if use else None
+            rst, ro, rl = O.reinsert_all(inst, parts[i], plens[i], removed[i], rks[i], g)
+            assert st[j] == rst, i
+            if rst == 0:
+                np.testing.assert_array_equal(l[j], rl, err_msg=str(i))
+                np.testing.assert_array_equal(o[j], ro, err_msg=str(i))
+            if use:
+                assert same_state(gens[j], g), i

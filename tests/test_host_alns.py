@@ -1,53 +1,36 @@
-"""Host-side ALNS pieces against the reference: removal cascade, destroy
-operators that need no schedule (random / worst / cluster / route), formulas."""
+"""Host-side ALNS pieces against the reference: the destroy oracle (the
+checker of K6) against the reference's destroy goldens, the formulas, and the
+construction helpers."""
 import numpy as np
 import pytest
 
 import inputs as I
 from conftest import config_instance
 from paper_2602_23685_b200 import alns as A
-from paper_2602_23685_b200 import insertion as INS
-from paper_2602_23685_b200.schedule import Solution
+from oracle import destroy_oracle as DO
 
 CID = {"gr17": 1, "eil51": 2, "kroA100": 3, "a280": 4, "dsj1000": 5}
 
 
-def test_remove_customers_matches_reference(golden, golden_meta):
-    for i, rec in enumerate(golden_meta["repairs"]):
-        inst = config_instance(rec["key"])
-        sol = Solution.from_arrays(golden[f"{rec['key']}/dec_ops"][rec["case"]],
-                                   golden[f"{rec['key']}/dec_lens"][rec["case"]])
-        tours, removed = INS.remove_customers(inst, sol, [int(x) for x in golden[f"repair/{i}/pick"]])
-        assert removed == list(golden[f"repair/{i}/removed"])
-        ops, lens = Solution.from_lists(tours).to_arrays(inst.n)
-        np.testing.assert_array_equal(lens, golden[f"repair/{i}/partial_lens"])
-        np.testing.assert_array_equal(ops, golden[f"repair/{i}/partial_ops"])
-
-
-def check_destroy(golden, golden_meta, operators):
-    seen = 0
+def test_oracle_destroy_matches_reference_goldens(golden, golden_meta):
+    """oracle/destroy_oracle.py (the CPU restatement the K6 tests check
+    against) reproduces the reference's destroy goldens for all six operators:
+    removed set, partial solution and final generator state."""
+    seen = set()
     for i, rec in enumerate(golden_meta["destroys"]):
-        if rec["operator"] not in operators:
-            continue
         inst = config_instance(rec["key"])
-        sol = Solution.from_arrays(golden[f"{rec['key']}/dec_ops"][rec["case"]],
-                                   golden[f"{rec['key']}/dec_lens"][rec["case"]])
+        ops, lens = golden[f"{rec['key']}/dec_ops"][rec["case"]], golden[f"{rec['key']}/dec_lens"][rec["case"]]
         rng = I.philox(41, CID[rec["key"]], rec["case"])
-        partial, removed = A.destroy(inst, sol, rec["operator"], rec["q"], rng)
+        po, pl, removed = DO.destroy(inst, ops, lens, rec["operator"], rec["q"], rng)
         assert removed == list(golden[f"destroy/{i}/removed"]), rec
-        ops, lens = partial.to_arrays(inst.n)
-        np.testing.assert_array_equal(lens, golden[f"destroy/{i}/lens"])
-        np.testing.assert_array_equal(ops, golden[f"destroy/{i}/ops"])
+        np.testing.assert_array_equal(pl, golden[f"destroy/{i}/lens"])
+        np.testing.assert_array_equal(po, golden[f"destroy/{i}/ops"][:2 * inst.n])
         st = rng.bit_generator.state
         assert [int(x) for x in st["state"]["counter"]] == rec["final_counter"]
         assert int(st["buffer_pos"]) == rec["final_buffer_pos"]
         assert int(st["has_uint32"]) == rec["final_has_uint32"]
-        seen += 1
-    assert seen
-
-
-def test_destroy_without_schedule_matches_reference(golden, golden_meta):
-    check_destroy(golden, golden_meta, ("random", "worst", "cluster", "route"))
+        seen.add(rec["operator"])
+    assert seen == set(A.DESTROY_OPERATORS)
 
 
 def test_formulas():  # test_alns.py:18-45
@@ -81,3 +64,42 @@ def test_sweep_order_is_permutation():
     inst = config_instance("eil51")
     order = A.sweep_order(inst)
     assert sorted(order) == list(inst.customers)
+
+
+def test_sweep_and_balance_match_reference_rules():
+    """sweep_order / _balance_sectors (numpy) against a direct statement of
+    the reference's rules (alns.py:290-327) on every config instance."""
+    from conftest import CONFIG_KEYS
+    for key in CONFIG_KEYS:
+        inst = config_instance(key)
+        d, p = inst.arrays()
+        cs = list(range(1, inst.n + 1))
+        a = max(cs, key=lambda c: (d[0][c], -c))
+        b = max(cs, key=lambda c: (d[a][c], -c))
+        assert A.sweep_order(inst) == sorted(cs, key=lambda c: (d[a][c] - d[b][c], d[0][c], c))
+        order = A.sweep_order(inst)
+        sectors = [order[v::inst.m] if v % 2 else order[v * len(order) // inst.m:(v + 1) * len(order) // inst.m]
+                   for v in range(inst.m)]
+        w = {c: 2.0 * d[0][c] + p[c] for c in cs}
+        secs = [list(x) for x in sectors]
+        loads = [sum(w[c] for c in x) for x in secs]
+        mean = sum(loads) / len(loads)
+        for _ in range(2 * inst.n):
+            if mean <= 0 or max(abs(x - mean) for x in loads) < 0.10 * mean:
+                break
+            hi = max(range(len(loads)), key=lambda i: loads[i])
+            lo = min(range(len(loads)), key=lambda i: loads[i])
+            if not secs[hi]:
+                break
+            bc, bp = None, max(loads)
+            for c in secs[hi]:
+                pk = max(loads[hi] - w[c], loads[lo] + w[c], *(loads[i] for i in range(len(loads)) if i not in (hi, lo)))
+                if pk < bp:
+                    bc, bp = c, pk
+            if bc is None:
+                break
+            secs[hi].remove(bc)
+            secs[lo].append(bc)
+            loads[hi] -= w[bc]
+            loads[lo] += w[bc]
+        assert A._balance_sectors(inst, sectors) == secs, key

@@ -173,3 +173,56 @@ def test_run_islands_world2_consistent():
     fit = O.decode_batch(inst, out[0]["genes"][None, :])["fitness"][0]
     assert fit == out[0]["best"]
     assert math.isfinite(fit)
+
+
+def _island_dev_vs_oracle(rank, world):
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).parent))
+    sys.path.insert(0, str(Path(__file__).parent / "golden"))
+    torch.cuda.set_device(0)  # both ranks share cuda:0; their kernels never wait on each other
+    from test_islands_gloo import OracleIslandEngine  # noqa
+    from paper_2602_23685_b200 import brkga as B
+    from paper_2602_23685_b200 import islands as IS
+    from paper_2602_23685_b200.configs import config_instance
+    inst = config_instance("eil51")
+    params = B.BrkgaParams(population=120, generations=12)
+    out = {}
+    for kind in ("device", "oracle"):
+        made = []
+
+        def factory(i, p, pop, g, kind=kind):
+            e = IS.DeviceIslandEngine(i, p, pop, g) if kind == "device" else OracleIslandEngine(i, p, pop, g)
+            made.append(e)
+            return e
+        genes, stats = IS.run_islands(inst, params, IS.IslandParams(migration_interval=3, migrants=5,
+                                                                    sync_interval=4),
+                                      seed=33, engine_factory=factory)
+        e = made[0]
+        out[kind] = {"best": stats.global_best, "winner": stats.winner, "island": stats.island_best,
+                     "genes": genes.cpu().numpy(), "trace": stats.trace, "migrations": stats.migrations,
+                     "pop": e.pop.cpu().numpy(), "fit": e.fit.cpu().numpy(),
+                     "key": e.gen.bit_generator.state["state"]["key"].tolist(),
+                     "counter": e.gen.bit_generator.state["state"]["counter"].tolist()}
+    return out
+
+
+@pytest.mark.gpu
+def test_device_island_engine_world2_equals_oracle_engine():
+    """DeviceIslandEngine (K3/K4 through the C-ABI) at world size 2 -- both
+    ranks on cuda:0 over gloo, device tensors staged through the host -- equals
+    the oracle engine on the same Philox streams: global best, winner,
+    broadcast chromosome, sync trace, and every island's final population
+    (which holds the migrated rows) and generator state."""
+    out = run_world(_island_dev_vs_oracle)
+    for r in (0, 1):
+        d, o = out[r]["device"], out[r]["oracle"]
+        assert d["best"] == o["best"] and d["winner"] == o["winner"] and d["island"] == o["island"]
+        assert d["trace"] == o["trace"] and d["migrations"] == o["migrations"] == 4
+        np.testing.assert_array_equal(d["genes"], o["genes"])
+        np.testing.assert_array_equal(d["pop"], o["pop"])
+        np.testing.assert_array_equal(d["fit"], o["fit"])
+    assert out[0]["device"]["best"] == out[1]["device"]["best"]
+    for r in (0, 1):
+        assert out[r]["device"]["counter"] == out[r]["oracle"]["counter"]
+    assert out[0]["device"]["key"] != out[1]["device"]["key"]  # independent island streams
