@@ -246,6 +246,187 @@ def extra_rates(device, ops, lens, decode_ms, n_dec, pipeline_seconds=30.0):
     return {k: round(v, 2) for k, v in out.items()}
 
 
+def l2_gather_ceiling():
+    """Measured random 4-byte gather rate of L2 (scripts/probes/l2gather.cu on
+    a B200 of this pool, profiles/r02_l2gather.json): the best rate over the
+    L2-resident table sizes (4-64 MB), G gathers/s."""
+    p = REPO / "profiles" / "r02_l2gather.json"
+    if not p.exists():
+        return None
+    rows = json.loads(p.read_text())["rows"]
+    return max(max(r["ggather_s"].values()) for r in rows if r["table_bytes"] <= (64 << 20))
+
+
+def k1_roofline(n, m, n_cand, ms_per_step, clocks):
+    """Roofline of K1 (the timed kernel) against three ceilings, per GPU:
+      issue     warp instructions per eval (ncu, profiles/k1_profile.json) x
+                evals/s vs 148 SMs x 4 schedulers x SM clock (measured median
+                under load) -- the binding ceiling of a dependent scalar replay;
+      l2_gather the 2n + m leg gathers d[prev][c] per eval (4 B each, random,
+                L2-resident int32 twin) vs the measured L2 gather ceiling;
+      hbm       ncu DRAM bytes per eval x evals/s vs the measured HBM copy peak.
+    The headline object is the ceiling with the largest fraction; the
+    algorithmic-bytes figure of SURVEY §8(d) (32n + 12m + 12 B/eval) is kept
+    beside it."""
+    evals_s = n_cand / (ms_per_step / 1e3)
+    hbm_peak, peak_kind = measured_peaks()
+    prof = {}
+    pp = REPO / "profiles" / "k1_profile.json"
+    if pp.exists():
+        prof = json.loads(pp.read_text())
+    sm_mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+    per_eval_alg = algorithmic_bytes_per_eval(n, m)
+    views = {}
+    if prof.get("warp_inst_per_eval"):
+        ach = prof["warp_inst_per_eval"] * evals_s / 1e9
+        pk = 148 * 4 * sm_mhz / 1e3
+        views["issue"] = {"achieved": round(ach, 1), "peak": round(pk, 1), "unit": "G warp-inst/s",
+                          "frac": round(ach / pk, 4), "per_eval": prof["warp_inst_per_eval"],
+                          "source": prof.get("source")}
+    l2 = l2_gather_ceiling()
+    if l2:
+        g = 2 * n + m
+        ach = g * evals_s / 1e9
+        views["l2_gather"] = {"achieved": round(ach, 1), "peak": round(l2, 1), "unit": "G gathers/s",
+                              "frac": round(ach / l2, 4), "per_eval": g,
+                              "source": "profiles/r02_l2gather.json (scripts/probes/l2gather.cu)"}
+    dram = prof.get("dram_bytes_per_eval")
+    if dram:
+        ach = dram * evals_s / 1e9
+        views["hbm"] = {"achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                        "frac": round(ach / hbm_peak, 4), "per_eval": dram, "peak_kind": peak_kind}
+    alg = per_eval_alg * evals_s / 1e9
+    bound = max(views, key=lambda k: views[k]["frac"]) if views else None
+    head = views.get(bound) if bound else {"achieved": round(alg, 1), "peak": hbm_peak, "unit": "GB/s",
+                                            "frac": round(alg / hbm_peak, 4)}
+    return {"bound": bound or "hbm", "achieved": head["achieved"], "peak": head["peak"],
+            "unit": head["unit"], "frac": head["frac"],
+            "traffic": round(dram * n_cand) if dram else None,
+            "traffic_source": "profiles/k1_profile.json: ncu dram__bytes_read+write per eval x candidates per launch",
+            "ceilings": views,
+            "algorithmic": {"bytes_per_eval": per_eval_alg, "achieved": round(alg, 1), "unit": "GB/s",
+                            "peak": hbm_peak, "frac": round(alg / hbm_peak, 4),
+                            "note": "SURVEY §8(d) bytes incl. L2-resident d/p gathers"},
+            "sm_mhz_used": sm_mhz}
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baselines(seconds: float = 6.0):
+    """The reference algorithms of the secondary rates, timed on this box's
+    host cores with the CPU oracle (C restatements of brkga.decode,
+    brkga.evolve and insertion.reinsert_all; kind "port"), each on a bounded
+    sample -- next to the GPU's decodes/s, generations/s and repairs/s."""
+    from concurrent.futures import ThreadPoolExecutor
+    import inputs as I
+    from oracle import oracle as O
+    from paper_2602_23685_b200.configs import config_instance
+    threads = O.default_threads()
+    out = {"cpu_model": cpu_model(), "cores": threads, "kind": "port"}
+    dsj = config_instance("dsj1000")
+    genes = I.chromosomes(dsj.n, 512, (136, 6001))
+    t0, done = time.perf_counter(), 0
+    while time.perf_counter() - t0 < seconds:
+        O.decode_batch(dsj, genes, threads=threads)
+        done += genes.shape[0]
+    out["decodes_per_s_dsj1000_random"] = round(done / (time.perf_counter() - t0), 2)
+    # evolve (numpy-Philox draws + [elite | mutant | offspring] build), one thread,
+    # paper population N_p = 30,000 at a280 (4n = 1116 genes)
+    a280 = config_instance("a280")
+    pop = I.chromosomes(a280.n, 30000, (136, 6002))
+    fit = np.random.default_rng(3).random(30000)
+    g = I.philox(136, 6003)
+    t0, gens = time.perf_counter(), 0
+    while time.perf_counter() - t0 < seconds / 2 or gens == 0:
+        pop = O.evolve(pop, fit, 0.15, 0.15, 0.7, g)
+        gens += 1
+    out["evolve_per_s_a280_Np30000_1thread"] = round(gens / (time.perf_counter() - t0), 3)
+    # reinsert_all at eil51 (q = 5 picked, cascade included), instances over threads
+    eil = config_instance("eil51")
+    dec = O.decode_batch(eil, I.chromosomes(eil.n, 256, (7, 7)))
+    cases = []
+    for i in range(256):
+        pick = I.philox(8, i).choice(np.arange(1, eil.n + 1), size=5, replace=False)
+        o, l, r = O.remove_customers(eil, dec["ops"][i], dec["lens"][i], pick)
+        cases.append((o[:2 * eil.n], l, r, (0, 2, 3, eil.m)[i % 4], i))
+
+    def one(c):
+        return O.reinsert_all(eil, c[0], c[1], c[2], c[3], I.philox(9, c[4]))[0]
+    t0, done = time.perf_counter(), 0
+    with ThreadPoolExecutor(threads) as ex:
+        while time.perf_counter() - t0 < seconds:
+            list(ex.map(one, cases))
+            done += len(cases)
+    out["alns_repairs_per_s_eil51"] = round(done / (time.perf_counter() - t0), 2)
+    return out
+
+
+def extra_distributed(dev, world, pipeline_seconds):
+    """Legs that run at every N (BASELINE configs 4 and 5): the a280 BRKGA
+    island model (N_p = 30,000 split over the ranks, ring migration of 32
+    elites every 10 generations, incumbent min-all-reduce) -- global
+    generations/s and the time of one migration + sync; and the dsj1000
+    time-budgeted pipeline on every rank with a final min-all-reduce of the
+    incumbent.  Times are max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2602_23685_b200 import brkga as B
+    from paper_2602_23685_b200 import islands as IS
+    from paper_2602_23685_b200 import rng as R
+    from paper_2602_23685_b200.configs import config_instance
+    rank = dist.get_rank() if world > 1 else 0
+
+    def tmax(x):
+        if world < 2:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+    out = {}
+    a280 = config_instance("a280")
+    size = 30000 // world
+    prm = B.BrkgaParams(population=size, generations=1)
+    gen = R.philox_generator(5, R.BRKGA_STREAM + rank)
+    eng = IS.DeviceIslandEngine(a280, prm, gen.random((size, 4 * a280.n)), gen)
+    for _ in range(2):
+        eng.generation()
+    G, gen_s, mig_s = 20, 0.0, 0.0
+    for g in range(1, G + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.generation()
+        torch.cuda.synchronize()
+        gen_s += time.perf_counter() - t0
+        if g % 10 == 0:
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            IS.migrate(eng, 32)
+            best, _, _ = IS.sync_incumbent(eng)
+            torch.cuda.synchronize()
+            mig_s += time.perf_counter() - t0
+    gen_s, mig_s = tmax(gen_s), tmax(mig_s)
+    out["islands_a280_generations_per_s_global_Np30000"] = round(G / gen_s, 2)
+    out["islands_a280_migration_plus_sync_ms"] = round(1e3 * mig_s / (G // 10), 3)
+    out["islands_a280_best_fitness"] = best
+    if pipeline_seconds > 0 and world > 1:
+        from paper_2602_23685_b200.pipeline import run_pipeline_budget_distributed
+        dsj = config_instance("dsj1000")
+        secs = 2 * pipeline_seconds
+        _, zb, tr = run_pipeline_budget_distributed(dsj, seconds=secs)
+        out[f"best_makespan_dsj1000_{secs:g}s_{world}gpu"] = zb
+        out["initial_makespan_dsj1000"] = tr[0][1]
+    return out
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -382,20 +563,7 @@ def run_gpu(args):
 
     line = None
     if rank == 0:
-        peak, peak_kind = measured_peaks()
-        per_eval = algorithmic_bytes_per_eval(n, m)
-        achieved = per_eval * n_cand / (ms_per_step / 1e3) / 1e9  # per GPU, dominant kernel
-        traffic = None
-        tp = REPO / "profiles" / "k1_traffic.json"
-        if tp.exists():  # ncu --set full capture of K1 (dram read+write), scaled per launch
-            per = json.loads(tp.read_text()).get("dram_bytes_per_eval")
-            traffic = None if per is None else round(per * n_cand)
-        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
-                "peak_kind": peak_kind, "bytes_per_eval": per_eval,
-                "traffic_source": "profiles/k1_traffic.json (ncu dram__bytes_read+write per eval x candidates)",
-                "note": "algorithmic bytes per SURVEY §8(d) (32n+12m+12); only the op stream "
-                        "is compulsory HBM traffic, d/p gathers are L2-resident"}
+        roof = k1_roofline(n, m, n_cand, ms_per_step, clk.summary())
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             import inputs as I
@@ -424,10 +592,41 @@ def run_gpu(args):
                 "setup_s": round(setup_s, 2)}
         if not args.no_extra and world == 1:
             line["extra"] = extra_rates(dev, ops, lens, decode_ms, n_cand, args.pipeline_seconds)
+            line["extra_cpu_baselines"] = cpu_baselines()
+    if not args.no_extra:
+        del ops, lens
+        torch.cuda.empty_cache()
+        dist_extra = extra_distributed(dev, world, args.pipeline_seconds)
+        if rank == 0:
+            line.setdefault("extra", {}).update(dist_extra)
+    if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without torchrun: re-launch this command under
+    torch.distributed.run with N local ranks (one per GPU, NCCL), so the
+    driver's plain invocation measures N GPUs.  Refuses when fewer than N GPUs
+    are visible (VRP_BENCH_SHARE_GPU=1: code-path test, ranks share GPUs)."""
+    import socket
+    import subprocess
+    if os.environ.get("VRP_BENCH_SHARE_GPU") != "1":
+        import torch
+        have = torch.cuda.device_count()
+        if have < n:
+            print(f"bench: --gpus {n} but only {have} GPU(s) visible", file=sys.stderr)
+            return 2
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -448,6 +647,11 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        raise SystemExit(spawn_ranks(args.gpus))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     else:
