@@ -30,6 +30,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "repair_core.cuh"
+#include "repair_team.cuh"
 #include "ddexp.cuh"
 
 namespace {
@@ -69,6 +70,10 @@ struct Dx {
     double *tw, *ready, *gains, *mind, *tdrop, *ret;
     int *dveh, *pveh, *flag, *mark, *list, *posd, *posp, *off;
 };
+
+__host__ __device__ inline size_t alns_scratch_bytes_dev(int n, int m) {
+    return make_layout(n, m).total + make_dlayout(n, m).total;
+}
 
 __device__ __forceinline__ Dx bind_dx(unsigned char *b, int n, int m) {
     const DLayout L = make_dlayout(n, m);
@@ -588,8 +593,10 @@ __device__ __noinline__ int replay_ool(const DevInstance &I, const int *row, int
 }
 __device__ __noinline__ void store_rows_ool(const Ctx &X, int *ops, int *lens) { store_rows(X, ops, lens); }
 
-template <bool INTD, bool SCAN>
-__global__ void __launch_bounds__(32)
+// TEAM: a CTA of TEAM_WARPS warps per worker -- warp 0 runs the iteration,
+// every warp joins the context rebuilds and the repair (repair_team.cuh).
+template <bool INTD, bool SCAN, bool TEAM = false>
+__global__ void __launch_bounds__(TEAM ? 32 * TEAM_WARPS : 32)
 alns_kernel(DevInstance I, vrp_alns_params P, vrp_alns_worker *__restrict__ workers, int32_t nw,
             int32_t *__restrict__ cur_ops, int32_t *__restrict__ cur_lens, int32_t *__restrict__ best_ops,
             int32_t *__restrict__ best_lens, const int32_t *__restrict__ q_draws, int64_t q_stride,
@@ -598,7 +605,9 @@ alns_kernel(DevInstance I, vrp_alns_params P, vrp_alns_worker *__restrict__ work
             int64_t rows_cap, unsigned char *__restrict__ scratch, size_t per) {
     __shared__ int s_len[MAXM];
     __shared__ vrp_alns_worker S;
-    const int lane = threadIdx.x;
+    __shared__ TeamCtl T;
+    __shared__ int s_nrem, s_rk;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int w = blockIdx.x;
     if (w >= nw) return;
     const int n = I.n, m = I.m, C = 2 * n + 2;
@@ -606,6 +615,12 @@ alns_kernel(DevInstance I, vrp_alns_params P, vrp_alns_worker *__restrict__ work
     Ctx X;
     bind_ctx(X, &I, b, s_len, lane);
     Dx D = bind_dx(b + make_layout(n, m).total, n, m);
+    UnitRes *units = nullptr;
+    UnitPick *picks = nullptr;
+    TeamWS W{};
+    GapRec *crecs = nullptr;
+    TeamCx cx{};
+    if (TEAM) W = bind_team(X, b + al8(alns_scratch_bytes_dev(n, m)), n, m, warp, nwarps, units, picks, crecs, cx);
 
     int32_t *cur = cur_ops + (int64_t)w * 2 * n, *clen = cur_lens + (int64_t)w * m;
     int32_t *best = best_ops + (int64_t)w * 2 * n, *blen = best_lens + (int64_t)w * m;
@@ -613,7 +628,7 @@ alns_kernel(DevInstance I, vrp_alns_params P, vrp_alns_worker *__restrict__ work
     long long tph[6] = {0, 0, 0, 0, 0, 0};  // destroy, rebuild, repair, replay, removed, options calls
 #endif
     PhiloxGen gen;
-    if (lane == 0) {
+    if (warp == 0 && lane == 0) {
         S = workers[w];
         gen.s = S.rng;
         S.n_trace = 0;
@@ -622,8 +637,10 @@ alns_kernel(DevInstance I, vrp_alns_params P, vrp_alns_worker *__restrict__ work
     __syncwarp();
 
     for (int64_t it = it_begin; it <= it_end; ++it) {
+        int dop = 0, rop = 0, q = 0, nrem = 0, rk = 0, st = 0;
+        double zc = 0.0;
+      if (warp == 0) {
         // operator selection (alns.py:567-571)
-        int dop = 0, rop = 0, q = 0;
         if (lane == 0) {
             dop = roulette(S.weights, 6, gen);
             rop = roulette(S.weights + 6, 4, gen);
@@ -657,13 +674,26 @@ alns_kernel(DevInstance I, vrp_alns_params P, vrp_alns_worker *__restrict__ work
         }
         VRP_TICK(0);
         // repair (alns.py:258-274): reinsert_all, then exact_makespan
-        rebuild_all<SCAN>(X);
-        const int nrem = compact_flags(X, D.flag);
-        const int rk = rop == 0 ? 0 : rop == 1 ? 2 : rop == 2 ? 3 : m;
-        VRP_TICK(1);
-        int st = reinsert_core<SCAN>(X, nrem, rk, &gen, true);
-        VRP_TICK(2);
-        double zc = 0.0;
+        rk = rop == 0 ? 0 : rop == 1 ? 2 : rop == 2 ? 3 : m;
+        if (!TEAM) {
+            rebuild_all<SCAN>(X);
+            nrem = compact_flags(X, D.flag);
+            VRP_TICK(1);
+            st = reinsert_core<SCAN>(X, nrem, rk, &gen, true);
+            VRP_TICK(2);
+        }
+      }
+        if (TEAM) {
+            __syncthreads();
+            rebuild_all_team(X, crecs, cx, warp, nwarps);
+            if (warp == 0) {
+                nrem = compact_flags(X, D.flag);
+                if (lane == 0) { s_nrem = nrem; s_rk = rk; }
+            }
+            __syncthreads();
+            st = reinsert_team(X, W, T, units, picks, crecs, cx, s_nrem, s_rk, &gen, true, warp, nwarps);
+        }
+      if (warp == 0) {
         if (!st) {
             const int *row = X.seq + (size_t)(lane < m ? lane : 0) * C;
             const int L = lane < m ? X.Lr[lane] : 0;
@@ -738,8 +768,9 @@ alns_kernel(DevInstance I, vrp_alns_params P, vrp_alns_worker *__restrict__ work
         if (acc) { if (SCAN) store_rows_ool(X, cur, clen); else store_rows(X, cur, clen); }
         if (nb) { if (SCAN) store_rows_ool(X, best, blen); else store_rows(X, best, blen); }
         __syncwarp();
+      }
     }
-    if (lane == 0) {
+    if (warp == 0 && lane == 0) {
         S.rng = gen.s;
         workers[w] = S;
 #ifdef VRP_PHASE_TIMERS  // debug builds: phase clocks into the trace buffer
@@ -829,7 +860,7 @@ gains_kernel(DevInstance I, const int32_t *__restrict__ ops, int64_t stride, con
 
 }  // namespace
 
-size_t alns_scratch_bytes(int n, int m) { return make_layout(n, m).total + make_dlayout(n, m).total; }
+size_t alns_scratch_bytes(int n, int m) { return alns_scratch_bytes_dev(n, m); }
 
 int launch_alns(const DevInstance &I, const vrp_alns_params &P, vrp_alns_worker *workers, int32_t nw,
                 int32_t *cur_ops, int32_t *cur_lens, int32_t *best_ops, int32_t *best_lens,
@@ -837,12 +868,14 @@ int launch_alns(const DevInstance &I, const vrp_alns_params &P, vrp_alns_worker 
                 int32_t *trace_it, double *trace_z, int64_t trace_cap, int32_t *rows_it,
                 double *rows_val, int64_t rows_cap, cudaStream_t stream) {
     if (nw <= 0 || it_end < it_begin) return 0;
-    const size_t per = al8(alns_scratch_bytes(I.n, I.m));
+    const bool team = use_team(I);
+    const size_t per = al8(alns_scratch_bytes(I.n, I.m)) + (team ? team_bytes(I.n, I.m, TEAM_WARPS) : 0);
     unsigned char *scratch = nullptr;
     if (cudaMallocAsync(&scratch, per * (size_t)nw, stream) != cudaSuccess) return -1;
 #define VRP_ALNS_ARGS I, P, workers, nw, cur_ops, cur_lens, best_ops, best_lens, q_draws, q_stride, it_begin, \
         it_end, trace_it, trace_z, trace_cap, rows_it, rows_val, rows_cap, scratch, per
-    if (use_scan(I)) alns_kernel<true, true><<<nw, 32, 0, stream>>>(VRP_ALNS_ARGS);
+    if (team) alns_kernel<true, true, true><<<nw, 32 * TEAM_WARPS, 0, stream>>>(VRP_ALNS_ARGS);
+    else if (use_scan(I)) alns_kernel<true, true><<<nw, 32, 0, stream>>>(VRP_ALNS_ARGS);
     else if (I.integral) alns_kernel<true, false><<<nw, 32, 0, stream>>>(VRP_ALNS_ARGS);
     else alns_kernel<false, false><<<nw, 32, 0, stream>>>(VRP_ALNS_ARGS);
 #undef VRP_ALNS_ARGS

@@ -11,6 +11,7 @@ struct vrp_instance {
     DevInstance dev;
     double *d = nullptr;
     int32_t *d32 = nullptr;
+    int32_t *d32t = nullptr;
     double *p = nullptr;
     int32_t *p32 = nullptr;
     int device = 0;
@@ -89,6 +90,13 @@ int vrp_instance_create(int32_t n, int32_t m, int32_t k, const double *d_host, c
         for (size_t i = 0; i < cells; ++i) tmp[i] = (int32_t)d_host[i];
         e = cudaMalloc(&h->d32, cells * sizeof(int32_t));
         if (e == cudaSuccess) e = cudaMemcpy(h->d32, tmp, cells * sizeof(int32_t), cudaMemcpyHostToDevice);
+        // the transpose: column c of d as a contiguous row (the repair scans read
+        // d[x][c] and d[c][x] for one c over every gap: two L1-resident rows)
+        const size_t W = (size_t)n + 1;
+        for (size_t a = 0; a < W; ++a)
+            for (size_t b = 0; b < W; ++b) tmp[b * W + a] = (int32_t)d_host[a * W + b];
+        if (e == cudaSuccess) e = cudaMalloc(&h->d32t, cells * sizeof(int32_t));
+        if (e == cudaSuccess) e = cudaMemcpy(h->d32t, tmp, cells * sizeof(int32_t), cudaMemcpyHostToDevice);
         for (int32_t i = 0; i <= n; ++i) tmp[i] = (int32_t)p_host[i];
         if (e == cudaSuccess) e = cudaMalloc(&h->p32, (size_t)(n + 1) * sizeof(int32_t));
         if (e == cudaSuccess) e = cudaMemcpy(h->p32, tmp, (size_t)(n + 1) * sizeof(int32_t), cudaMemcpyHostToDevice);
@@ -99,7 +107,7 @@ int vrp_instance_create(int32_t n, int32_t m, int32_t k, const double *d_host, c
         return cuda_fail(e, "vrp_instance_create");
     }
     h->dev.n = n; h->dev.m = m; h->dev.k = k; h->dev.W = n + 1;
-    h->dev.d = h->d; h->dev.d32 = h->d32; h->dev.p = h->p; h->dev.p32 = h->p32;
+    h->dev.d = h->d; h->dev.d32 = h->d32; h->dev.d32t = h->d32t; h->dev.p = h->p; h->dev.p32 = h->p32;
     h->dev.integral = integral ? 1 : 0;
     *out = h;
     return 0;
@@ -109,6 +117,7 @@ int vrp_instance_destroy(vrp_instance_t h) {
     if (!h) return 0;
     if (h->d) cudaFree(h->d);
     if (h->d32) cudaFree(h->d32);
+    if (h->d32t) cudaFree(h->d32t);
     if (h->p) cudaFree(h->p);
     if (h->p32) cudaFree(h->p32);
     delete h;

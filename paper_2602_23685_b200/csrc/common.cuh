@@ -10,6 +10,7 @@ struct DevInstance {
     int32_t n, m, k, W;       // W = n + 1 (row pitch of d)
     const double *d;          // (n+1)^2 fp64
     const int32_t *d32;       // same values as int32 when `integral`, else null
+    const int32_t *d32t;      // its transpose (d32t[b*W + a] = d[a][b]) when `integral`, else null
     const double *p;          // n+1 fp64
     const int32_t *p32;       // same values as int32 when `integral`, else null
     int32_t integral;         // every d and p entry is an integer in [0, 2^31)

@@ -28,6 +28,7 @@
 #include "kernels.h"
 
 #include "repair_core.cuh"
+#include "repair_team.cuh"
 
 namespace {
 
@@ -104,6 +105,93 @@ repair_kernel(DevInstance I, const int32_t *__restrict__ pops, int64_t pstride,
     }
 }
 
+// The same repair with a CTA of TEAM_WARPS warps per instance (repair_team.cuh):
+// integral instances with long routes (use_scan).
+__global__ void __launch_bounds__(32 * TEAM_WARPS)
+repair_team_kernel(DevInstance I, const int32_t *__restrict__ pops, int64_t pstride,
+                   const int32_t *__restrict__ plens, const int32_t *__restrict__ removed, int64_t rstride,
+                   const int32_t *__restrict__ nremoved, const int32_t *__restrict__ regret_k,
+                   vrp_philox *__restrict__ states, int32_t *__restrict__ out_ops, int64_t ostride,
+                   int32_t *__restrict__ out_lens, int32_t *__restrict__ status,
+                   unsigned char *__restrict__ scratch, size_t per, int64_t N) {
+    __shared__ int s_len[MAXM];
+    __shared__ TeamCtl T;
+    __shared__ int s_bad, s_nrem;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t inst = blockIdx.x;
+    if (inst >= N) return;
+    const int n = I.n, m = I.m;
+    const Layout Ly = make_layout(n, m);
+    unsigned char *b = scratch + (size_t)inst * per;
+    Ctx X;
+    bind_ctx(X, &I, b, s_len, lane);
+    UnitRes *units;
+    UnitPick *picks;
+    GapRec *crecs;
+    TeamCx cx;
+    TeamWS W = bind_team(X, b + al8(Ly.total), n, m, warp, nw, units, picks, crecs, cx);
+    const bool use_rng = states != nullptr;
+    PhiloxGen gen;
+    if (warp == 0) {
+        const int32_t *po = pops + inst * pstride;
+        const int32_t *pl = plens + inst * m;
+        if (lane < m) s_len[lane] = pl[lane];
+        __syncwarp();
+        int off = 0;
+        bool bad = false;
+        for (int v = 0; v < m; ++v) {
+            const int L = s_len[v];
+            bad |= L < 0 || off + L > 2 * n;
+            if (!bad)
+                for (int i = lane; i < L; i += 32) {
+                    const int op = po[off + i];
+                    bad |= op < 0 || op >= 2 * n;
+                    X.seq[(size_t)v * X.C + i] = op;
+                }
+            off += L > 0 ? L : 0;
+        }
+        bad = __any_sync(VRP_FULL_MASK, bad);
+        if (lane == 0) s_bad = bad;
+        if (use_rng && lane == 0) gen.s = states[inst];
+    }
+    __syncthreads();
+    int st = 0;
+    if (s_bad) {
+        st = 2;
+    } else {
+        rebuild_all_team(X, crecs, cx, warp, nw);
+        if (warp == 0) {
+            for (int c = lane; c <= n; c += 32) X.s_has[c] = 0;
+            __syncwarp();
+            const int nr = nremoved[inst];
+            for (int i = lane; i < nr; i += 32) {
+                const int c = removed[inst * rstride + i];
+                if (c >= 1 && c <= n) X.s_has[c] = 1;
+            }
+            __syncwarp();
+            const int nrem = compact_flags(X, X.s_has);
+            if (lane == 0) s_nrem = nrem;
+        }
+        __syncthreads();
+        st = reinsert_team(X, W, T, units, picks, crecs, cx, s_nrem, regret_k[inst], &gen, use_rng, warp, nw);
+    }
+    if (warp == 0) {
+        int32_t *oo = out_ops + inst * ostride;
+        int off = 0;
+        for (int v = 0; v < m; ++v) {
+            const int L = st ? 0 : s_len[v];
+            for (int i = lane; i < L; i += 32) oo[off + i] = X.seq[(size_t)v * X.C + i];
+            off += L;
+        }
+        for (int i = off + lane; i < 2 * n; i += 32) oo[i] = -1;
+        if (lane < m) out_lens[inst * m + lane] = st ? 0 : s_len[lane];
+        if (lane == 0) {
+            status[inst] = st;
+            if (use_rng) states[inst] = gen.s;
+        }
+    }
+}
+
 }  // namespace
 
 size_t repair_scratch_bytes(int n, int m) { return make_layout(n, m).total; }
@@ -113,6 +201,17 @@ int launch_repair(const DevInstance &I, const int32_t *pops, int64_t pstride, co
                   const int32_t *regret_k, vrp_philox *states, int32_t *out_ops, int64_t ostride,
                   int32_t *out_lens, int32_t *status, int64_t N, cudaStream_t stream) {
     if (N <= 0) return 0;
+    if (use_team(I)) {
+        const size_t per = al8(make_layout(I.n, I.m).total) + team_bytes(I.n, I.m, TEAM_WARPS);
+        unsigned char *scratch = nullptr;
+        if (cudaMallocAsync(&scratch, per * (size_t)N, stream) != cudaSuccess) return -1;
+        repair_team_kernel<<<(unsigned)N, 32 * TEAM_WARPS, 0, stream>>>(I, pops, pstride, plens, removed, rstride,
+                                                                      nremoved, regret_k, states, out_ops, ostride,
+                                                                      out_lens, status, scratch, per, N);
+        const cudaError_t e = cudaPeekAtLastError();
+        cudaFreeAsync(scratch, stream);
+        return e == cudaSuccess ? 0 : -1;
+    }
     const size_t per = make_layout(I.n, I.m).total;
     unsigned char *scratch = nullptr;
     if (cudaMallocAsync(&scratch, per * (size_t)N, stream) != cudaSuccess) return -1;
