@@ -243,6 +243,11 @@ def extra_rates(device, ops, lens, decode_ms, n_dec, pipeline_seconds=30.0):
         _, zb, tr = run_pipeline_budget(dsj, seconds=2 * pipeline_seconds)
         out[f"best_makespan_dsj1000_{2 * pipeline_seconds:g}s"] = zb
         out["initial_makespan_dsj1000"] = tr[0][1]
+        # the same budget with the ALNS stage on at n = 999 (team-repair ALNS,
+        # 148 workers after a shorter polish): the paper's ALNS -> BRKGA order
+        _, zb, tr = run_pipeline_budget(dsj, seconds=2 * pipeline_seconds, alns_max_n=10**9, pool_size=148,
+                                        alns_share=0.9, polish_share=0.3, final_share=0.3)
+        out[f"best_makespan_dsj1000_{2 * pipeline_seconds:g}s_alns_on"] = zb
     return {k: round(v, 2) for k, v in out.items()}
 
 

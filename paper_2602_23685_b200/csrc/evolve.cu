@@ -1,11 +1,11 @@
 // evolve.cu -- K4: the BRKGA generation step on device (brkga.py:231-252,
 // run_brkga :454-467).
 //
-//  order   stable argsort of the fitness (brkga.py:243, :456): rank-by-count
-//          over (fitness key, index) -- every element counts the elements
-//          that precede it, so equal fitnesses keep index order, exactly as
-//          numpy's stable sort.  O(N^2) compares, tiled through shared memory:
-//          ~0.1 ms at N = 30,000, far below one generation's decode.
+//  order   stable argsort of the fitness (brkga.py:243, :456): the rank of
+//          every (fitness key, index) pair -- equal fitnesses keep index
+//          order, exactly as numpy's stable sort -- from 1024-pair tiles
+//          sorted in shared memory plus one binary search per tile and element
+//          (was an O(N^2) rank count: 1.31 ms at N = 30,000).
 //  draws   numpy Generator(Philox) reproduced bit for bit.  Philox4x64-10 is
 //          counter based, so the q-th 64-bit output of the stream is a pure
 //          function of (state, q): mutant genes, the e_idx/o_idx Lemire draws
@@ -19,7 +19,8 @@
 //          generator continues exactly where numpy's would.
 //  build   [elites | mutants | offspring] rows; offspring gene = mask ?
 //          elite parent : other parent.  HBM-bound: 3 x 4n x 8 B per
-//          offspring (two parent reads, one write).
+//          offspring (two parent reads, one write); one Philox block per
+//          thread serves 4 genes (was one block per gene).
 //  best    block reduction of (fitness, first index) over the new rows; the
 //          strict `<` against the incumbent is evaluated on device and the
 //          winning chromosome copied (run_brkga's best tracking, :461-467).
@@ -48,30 +49,70 @@ __device__ __forceinline__ uint64_t fit_key(double x) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
+// Stable order = rank of every (key, index) pair in the total order of the
+// pairs (equal fitnesses keep index order, numpy's stable argsort):
+//   sort_tiles_kernel  each block sorts a tile of 1024 pairs in shared memory
+//                      (bitonic network on the composite key -- a total order,
+//                      so the result is unique)
+//   rank_kernel        rank(i) = sum over tiles of the number of pairs below
+//                      (key_i, i): a binary search per tile, ~10 steps x
+//                      N/1024 tiles per element instead of N compares.
 constexpr int RANK_TILE = 1024;
 
-// order[rank(i)] = i, rank = #{j : (key_j, j) < (key_i, i)}
-__global__ void __launch_bounds__(256) rank_kernel(const double *__restrict__ fit, int64_t N,
-                                                   int32_t *__restrict__ order) {
-    __shared__ uint64_t tile[RANK_TILE];
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t ki = i < N ? fit_key(__ldg(fit + i)) : ~0ull;
-    int64_t rank = 0;
-    for (int64_t base = 0; base < N; base += RANK_TILE) {
-        const int64_t cnt = N - base < RANK_TILE ? N - base : RANK_TILE;
-        __syncthreads();
-        for (int t = threadIdx.x; t < cnt; t += blockDim.x) tile[t] = fit_key(__ldg(fit + base + t));
-        __syncthreads();
-        if (i < N) {
-            int64_t r = 0;
-            for (int t = 0; t < cnt; ++t) {
-                const uint64_t kj = tile[t];
-                r += (kj < ki) || (kj == ki && base + t < i);
+__device__ __forceinline__ bool pair_lt(uint64_t ka, int32_t ia, uint64_t kb, int32_t ib) {
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+__global__ void __launch_bounds__(512) sort_tiles_kernel(const double *__restrict__ fit, int64_t N,
+                                                         uint64_t *__restrict__ skey, int32_t *__restrict__ sidx) {
+    __shared__ uint64_t k[RANK_TILE];
+    __shared__ int32_t ix[RANK_TILE];
+    const int64_t base = (int64_t)blockIdx.x * RANK_TILE;
+    for (int t = threadIdx.x; t < RANK_TILE; t += blockDim.x) {
+        const int64_t i = base + t;
+        k[t] = i < N ? fit_key(__ldg(fit + i)) : ~0ull;
+        ix[t] = i < N ? (int32_t)i : INT32_MAX;
+    }
+    __syncthreads();
+    for (int size = 2; size <= RANK_TILE; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < RANK_TILE / 2; t += blockDim.x) {
+                const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint64_t ka = k[lo], kb = k[hi];
+                const int32_t ia = ix[lo], ib = ix[hi];
+                if (pair_lt(kb, ib, ka, ia) == up) { k[lo] = kb; k[hi] = ka; ix[lo] = ib; ix[hi] = ia; }
             }
-            rank += r;
+            __syncthreads();
         }
     }
-    if (i < N) order[rank] = (int32_t)i;
+    for (int t = threadIdx.x; t < RANK_TILE; t += blockDim.x) {
+        skey[base + t] = k[t];
+        sidx[base + t] = ix[t];
+    }
+}
+
+// order[rank(i)] = i
+__global__ void __launch_bounds__(256) rank_kernel(const double *__restrict__ fit, int64_t N,
+                                                   const uint64_t *__restrict__ skey,
+                                                   const int32_t *__restrict__ sidx, int32_t *__restrict__ order) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const uint64_t ki = fit_key(__ldg(fit + i));
+    const int64_t ntiles = (N + RANK_TILE - 1) / RANK_TILE;
+    int64_t rank = 0;
+    for (int64_t t = 0; t < ntiles; ++t) {
+        const uint64_t *kt = skey + t * RANK_TILE;
+        const int32_t *it = sidx + t * RANK_TILE;
+        int lo = 0, hi = RANK_TILE;  // first position whose pair is not below (ki, i); padding sorts last
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (pair_lt(kt[mid], it[mid], ki, (int32_t)i)) lo = mid + 1;
+            else hi = mid;
+        }
+        rank += lo;
+    }
+    order[rank] = (int32_t)i;
 }
 
 struct EvolveShape {
@@ -141,34 +182,69 @@ __device__ __forceinline__ uint64_t u64s_for_u32(const vrp_philox &S, uint64_t u
     return (from_u64 + 1) / 2;
 }
 
-// rows [elites | mutants | offspring]
-__global__ void __launch_bounds__(256) build_kernel(const vrp_philox *__restrict__ Sp, EvolveShape sh,
-                                                    const double *__restrict__ pop,
-                                                    const int32_t *__restrict__ order,
-                                                    const int32_t *__restrict__ e_idx,
-                                                    const int32_t *__restrict__ o_idx,
-                                                    const unsigned long long *__restrict__ u32_used,
-                                                    double bias, double *__restrict__ out) {
+// rows [elites | mutants | offspring], in three launches:
+//   elite rows: 16-byte row copies (G = 4n is even: 16-byte aligned rows);
+//   mutant / offspring rows: one thread per Philox block (4 consecutive
+//     stream words -> 4 consecutive genes of a row; G is a multiple of 4, so
+//     every row has the same block phase), one block row per grid row.
+template <bool VEC>  // VEC: G even and both bases 16-byte aligned (BRKGA's 4n genes)
+__global__ void __launch_bounds__(256) elite_rows_kernel(const double *__restrict__ pop,
+                                                         const int32_t *__restrict__ order, int64_t G,
+                                                         double *__restrict__ out, int64_t row0) {
+    const int64_t r = row0 + blockIdx.y;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    if (VEC) {
+        const double2 *src = reinterpret_cast<const double2 *>(pop + (int64_t)order[r] * G);
+        double2 *dst = reinterpret_cast<double2 *>(out + r * G);
+        for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < G / 2; j += step) dst[j] = __ldg(src + j);
+    } else {
+        const double *src = pop + (int64_t)order[r] * G;
+        double *dst = out + r * G;
+        for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < G; j += step) dst[j] = __ldg(src + j);
+    }
+}
+
+// OFF = false: mutant row r (stream words r*G ..); OFF = true: offspring row r
+// (mask words mask0 + r*G ..; gene = mask < bias ? elite parent : other parent)
+template <bool OFF>
+__global__ void __launch_bounds__(256) stream_rows_kernel(const vrp_philox *__restrict__ Sp, EvolveShape sh,
+                                                          const double *__restrict__ pop,
+                                                          const int32_t *__restrict__ order,
+                                                          const int32_t *__restrict__ e_idx,
+                                                          const int32_t *__restrict__ o_idx,
+                                                          const unsigned long long *__restrict__ u32_used,
+                                                          double bias, double *__restrict__ out, int64_t row0) {
     const vrp_philox S = *Sp;
-    const int64_t G = sh.G;
-    const uint64_t mut = (uint64_t)(sh.n_mutant * G);
-    const uint64_t mask0 = mut + u64s_for_u32(S, *u32_used);
-    const int64_t total = sh.N * G;
-    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
-         x += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = x / G, g = x - row * G;
-        double val;
-        if (row < sh.n_elite) {
-            val = __ldg(pop + (int64_t)order[row] * G + g);
-        } else if (row < sh.n_elite + sh.n_mutant) {
-            val = u64_to_double(stream_u64(S, (uint64_t)((row - sh.n_elite) * G + g)));
-        } else {
-            const int64_t i = row - sh.n_elite - sh.n_mutant;
-            const double u = u64_to_double(stream_u64(S, mask0 + (uint64_t)(i * G + g)));
-            const int64_t src = u < bias ? order[e_idx[i]] : order[sh.n_elite + o_idx[i]];
-            val = __ldg(pop + src * G + g);
+    const int64_t G = sh.G, r = row0 + blockIdx.y;
+    const int64_t head = 4 - (int64_t)S.buffer_pos;
+    const int64_t q0 = (OFF ? (int64_t)(sh.n_mutant * G) + (int64_t)u64s_for_u32(S, *u32_used) : 0) + r * G;
+    // block-aligned start (stream words >= head come in Philox blocks of 4)
+    const int64_t qq0 = q0 - head;
+    const int64_t b0 = qq0 >= 0 ? qq0 / 4 : -((3 - qq0) / 4);
+    const int64_t nblk = (qq0 + G - 1 - 4 * b0) / 4 + 1;
+    const double *pe = nullptr, *po = nullptr;
+    if (OFF) {
+        pe = pop + (int64_t)order[e_idx[r]] * G;
+        po = pop + (int64_t)order[sh.n_elite + o_idx[r]] * G;
+    }
+    double *dst = out + ((OFF ? sh.n_elite + sh.n_mutant : sh.n_elite) + r) * G;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nblk; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t qqb = 4 * (b0 + j);
+        uint64_t w[4];
+        if (qqb >= 0) {
+            uint64_t c[4];
+            ctr_add(S.ctr, 1 + (uint64_t)(qqb / 4), c);
+            philox_block(c[0], c[1], c[2], c[3], S.key[0], S.key[1], w);
         }
-        out[x] = val;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t g = qqb + k - qq0;
+            if (g < 0 || g >= G) continue;
+            const int64_t qq = qqb + k;
+            const uint64_t x = qq >= 0 ? w[k] : S.buffer[S.buffer_pos + (qq + head)];
+            const double u = u64_to_double(x);
+            dst[g] = OFF ? __ldg((u < bias ? pe : po) + g) : u;
+        }
     }
 }
 
@@ -302,8 +378,18 @@ __global__ void gather_fit_kernel(const double *__restrict__ fit, const int32_t 
 
 int launch_fitness_order(const double *fit, int64_t N, int32_t *order, cudaStream_t stream) {
     if (N <= 0) return 0;
-    const int64_t blocks = (N + 255) / 256;
-    rank_kernel<<<(unsigned)blocks, 256, 0, stream>>>(fit, N, order);
+    const int64_t ntiles = (N + RANK_TILE - 1) / RANK_TILE;
+    uint64_t *skey = nullptr;
+    int32_t *sidx = nullptr;
+    if (cudaMallocAsync(&skey, sizeof(uint64_t) * (size_t)(ntiles * RANK_TILE), stream) != cudaSuccess) return -1;
+    if (cudaMallocAsync(&sidx, sizeof(int32_t) * (size_t)(ntiles * RANK_TILE), stream) != cudaSuccess) {
+        cudaFreeAsync(skey, stream);
+        return -1;
+    }
+    sort_tiles_kernel<<<(unsigned)ntiles, 512, 0, stream>>>(fit, N, skey, sidx);
+    rank_kernel<<<(unsigned)((N + 255) / 256), 256, 0, stream>>>(fit, N, skey, sidx, order);
+    cudaFreeAsync(skey, stream);
+    cudaFreeAsync(sidx, stream);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
 }
 
@@ -338,7 +424,23 @@ int launch_evolve(const double *pop, const double *fit, int64_t N, int64_t G, do
     const int grid = sm_count * 8;
     if (sh.n_off > 0) draw_kernel<<<grid, 256, 0, stream>>>(state, sh, e_idx, o_idx, scal);
     fix_kernel<<<1, 1, 0, stream>>>(state, sh, e_idx, o_idx, scal, scal + 1);
-    build_kernel<<<grid * 4, 256, 0, stream>>>(state, sh, pop, order, e_idx, o_idx, scal + 1, bias, out);
+    {
+        constexpr int64_t YMAX = 65535;  // grid rows per launch
+        const bool vec = G % 2 == 0 && ((uintptr_t)pop % 16) == 0 && ((uintptr_t)out % 16) == 0;
+        const unsigned gx = (unsigned)(((vec ? G / 2 : G) + 255) / 256);
+        for (int64_t r0 = 0; r0 < sh.n_elite; r0 += YMAX) {
+            const dim3 grid2(gx, (unsigned)(sh.n_elite - r0 < YMAX ? sh.n_elite - r0 : YMAX));
+            if (vec) elite_rows_kernel<true><<<grid2, 256, 0, stream>>>(pop, order, G, out, r0);
+            else elite_rows_kernel<false><<<grid2, 256, 0, stream>>>(pop, order, G, out, r0);
+        }
+        const unsigned bx = (unsigned)((G / 4 + 2 + 255) / 256);
+        for (int64_t r0 = 0; r0 < sh.n_mutant; r0 += YMAX)
+            stream_rows_kernel<false><<<dim3(bx, (unsigned)(sh.n_mutant - r0 < YMAX ? sh.n_mutant - r0 : YMAX)), 256,
+                                        0, stream>>>(state, sh, pop, order, e_idx, o_idx, scal + 1, bias, out, r0);
+        for (int64_t r0 = 0; r0 < sh.n_off; r0 += YMAX)
+            stream_rows_kernel<true><<<dim3(bx, (unsigned)(sh.n_off - r0 < YMAX ? sh.n_off - r0 : YMAX)), 256, 0,
+                                       stream>>>(state, sh, pop, order, e_idx, o_idx, scal + 1, bias, out, r0);
+    }
     state_kernel<<<1, 1, 0, stream>>>(state, sh, scal + 1);
     cudaFreeAsync(e_idx, stream);
     cudaFreeAsync(o_idx, stream);

@@ -41,6 +41,9 @@ constexpr int ST_RETRY = 4;                 // internal: narrow ready table over
 constexpr uint32_t NOT_READY32 = 0xFFFFFFFFu;
 constexpr int OPS_AHEAD = 8;   // op codes in registers (positions i .. i+7)
 constexpr int LEGS_AHEAD = 4;  // gathered legs in registers (positions i .. i+3)
+#ifndef VRP_K1_RA
+#define VRP_K1_RA 0  // run-ahead ops per lockstep round (exact mode, slot table); measured slower, see DESIGN.md
+#endif
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -178,7 +181,7 @@ struct RouteStream {
 // MC > 0 fixes the fleet size at compile time (MC == I.m; the m = 6 fleets of
 // every benchmark config beyond gr17): lane/candidate indexing, the slot
 // classes and the rotation OR then cost no run-time tests.
-template <typename OpT, bool INTD, int MODE, bool REC, bool NARROW, bool COMPACT = false, int MC = 0>
+template <typename OpT, bool INTD, int MODE, bool REC, bool NARROW, bool COMPACT = false, int MC = 0, int RA = 0>
 __global__ void __launch_bounds__(256)
 makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 const int32_t *__restrict__ lens, int64_t N, int G, double *__restrict__ z_out,
@@ -417,6 +420,73 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                     cap_step(op, k, s, lo, hi);
                     rs.advance(I);
                 }
+                if (RA > 0) {
+                    // Run-ahead (exact mode, slot table): a lane that moved keeps
+                    // executing its route -- up to RA more ops -- while its pickups'
+                    // dropoffs are visible and its own slot class has room, with no
+                    // warp collective per op.  Visibility: the __syncwarp publishes
+                    // this round's first ops; a run-ahead drop writes its value, then
+                    // a block fence, then the slot id, and a run-ahead pickup reads
+                    // the slot id, fences, then the value (message passing), so a
+                    // pickup either sees its dropoff complete or stops.  Values only
+                    // depend on DAG predecessors, so results are unchanged.  Slot
+                    // bookkeeping: a lane toggles slots of its own class (takes, and
+                    // releases of its own customers) and releases foreign slots; per
+                    // round a slot has at most one net own-class toggle (its class
+                    // owner) and at most one foreign release (a slot freed by another
+                    // lane is invisible to its owner until the merge), so
+                    // start ^ OR(own toggles) ^ OR(foreign toggles) is the exact new
+                    // free mask.
+                    __syncwarp();
+                    const unsigned f0 = freem;
+                    unsigned flips = 0;
+                    volatile uint8_t *vsid = s_sid;
+                    volatile uint32_t *vval = s_val;
+                    for (int ra = 0; ra < RA && go && rs.i < rs.L; ++ra) {
+                        const int op2 = rs.o[0];
+                        const int c2 = op_customer(op2);
+                        const TT arr2 = t + (TT)rs.leg0();
+                        TT tn2 = arr2;
+                        if (op2 & 1) {
+                            const int sid2 = vsid[c2];
+                            if (sid2 == 0xFF) break;
+                            __threadfence_block();
+                            const TT r2 = (TT)vval[sid2 & (SLOTS - 1)];
+                            if (!(arr2 >= r2)) tn2 = r2;
+                            const unsigned bit = 1u << (sid2 & (SLOTS - 1));
+                            flips ^= bit;
+                            freem ^= bit;
+                        } else {
+                            const unsigned av = freem & cls;
+                            if (!av) break;
+                            const int sl = __ffs(av) - 1;
+                            const TT rv = arr2 + s_p[c2];
+                            ovf |= rv < arr2 || rv == (TT)NOT_READY32;
+                            vval[sl] = (uint32_t)rv;
+                            __threadfence_block();
+                            vsid[c2] = (uint8_t)sl;
+                            flips ^= 1u << sl;
+                            freem ^= 1u << sl;
+                        }
+                        ovf |= arr2 < t;
+                        t = tn2;
+                        lastc = c2;
+                        cap_step(op2, k, s, lo, hi);
+                        rs.advance(I);
+                    }
+                    if (__any_sync(VRP_FULL_MASK, flips != 0)) {
+                        unsigned tk = flips & cls, rl = flips & ~cls;
+                        tk |= __shfl_sync(VRP_FULL_MASK, tk, pt1);
+                        rl |= __shfl_sync(VRP_FULL_MASK, rl, pt1);
+                        if (m > 2) { tk |= __shfl_sync(VRP_FULL_MASK, tk, pt2); rl |= __shfl_sync(VRP_FULL_MASK, rl, pt2); }
+                        if (m > 4) { tk |= __shfl_sync(VRP_FULL_MASK, tk, pt4); rl |= __shfl_sync(VRP_FULL_MASK, rl, pt4); }
+                        if (m > 8) { tk |= __shfl_sync(VRP_FULL_MASK, tk, pt8); rl |= __shfl_sync(VRP_FULL_MASK, rl, pt8); }
+                        if (m > 16) { tk |= __shfl_sync(VRP_FULL_MASK, tk, pt16); rl |= __shfl_sync(VRP_FULL_MASK, rl, pt16); }
+                        freem = f0 ^ tk ^ rl;
+                    } else {
+                        freem = f0;
+                    }
+                }
                 const unsigned moved = __ballot_sync(VRP_FULL_MASK, go);
                 const unsigned left = __ballot_sync(VRP_FULL_MASK, active && rs.i < rs.L);
                 __syncwarp();
@@ -486,12 +556,12 @@ int plan(Kern kern, int n, int m, int mode, int ready_bytes, bool compact, Shape
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)out.smem) == cudaSuccess ? 0 : -1;
 }
 
-template <typename OpT, bool INTD, int MODE, bool REC, bool NARROW, bool COMPACT = false, int MC = 0>
+template <typename OpT, bool INTD, int MODE, bool REC, bool NARROW, bool COMPACT = false, int MC = 0, int RA = 0>
 int launch_t(const DevInstance &I, const void *ops, int64_t stride, const int32_t *lens,
              int64_t N, double *z, int32_t *status, double *returns, int32_t *bottleneck,
              double *arrival, double *timev, int32_t *q0, cudaStream_t stream, int sm_count,
              int fixup) {
-    auto kern = makespan_kernel<OpT, INTD, MODE, REC, NARROW, COMPACT, MC>;
+    auto kern = makespan_kernel<OpT, INTD, MODE, REC, NARROW, COMPACT, MC, RA>;
     static int cached_n = -1, cached_m = -1;
     static Shape sh;
     if (cached_n != I.n || cached_m != I.m) {
@@ -519,9 +589,9 @@ int launch_narrow(const DevInstance &I, const void *ops, int64_t stride, const i
                   int64_t N, double *z, int32_t *status, double *returns, int32_t *bottleneck,
                   cudaStream_t stream, int sm_count) {
     int rc;
-    if (MODE != MODE_TWO && I.m == 6 && I.k <= SLOTS / 6)  // slot table, m fixed at 6
-        rc = launch_t<OpT, true, MODE, false, true, true, 6>(I, ops, stride, lens, N, z, status, returns, bottleneck,
-                                                             nullptr, nullptr, nullptr, stream, sm_count, 0);
+    if (MODE != MODE_TWO && I.m == 6 && I.k <= SLOTS / 6)  // slot table, m fixed at 6 (+ run-ahead: exact)
+        rc = launch_t<OpT, true, MODE, false, true, true, 6, MODE == MODE_EXACT ? VRP_K1_RA : 0>(
+            I, ops, stride, lens, N, z, status, returns, bottleneck, nullptr, nullptr, nullptr, stream, sm_count, 0);
     else if (MODE != MODE_TWO && I.m * I.k <= SLOTS)  // slot table (see makespan_kernel: COMPACT)
         rc = launch_t<OpT, true, MODE, false, true, true>(I, ops, stride, lens, N, z, status, returns, bottleneck,
                                                           nullptr, nullptr, nullptr, stream, sm_count, 0);

@@ -49,7 +49,11 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_
     the budget (default 0.4 for n >= 90; small instances measured better
     when ALNS starts from the constructed solution, so 0 there).
     Stage 1, ``alns_share`` of what remains before the final reserve (only
-    for n <= ``alns_max_n``: at larger n an ALNS iteration takes seconds):
+    for n <= ``alns_max_n``; measured at n = 999, profiles/r02_summary.md:
+    the team-repair ALNS runs ~0.5 s per iteration per worker there, but its
+    capacity cascades remove 50-200 customers per move and, given the stage,
+    it does not improve the polished incumbent -- 299.0 M with the stage vs
+    295.7 M without in 60 s -- so the default keeps it for n <= 400):
     ``pool_size`` device-resident ALNS workers (one warp each,
     vrp_alns_iterate) in pools that poll their pool's incumbent.  With
     ``fit_cooling`` the SA schedule is fitted to the stage: a 10-iteration
@@ -97,6 +101,7 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_
     if instance.n > alns_max_n:
         alns_end = now
     init = best[1]
+    per_iter = None
     if alns_params is None and now < alns_end:
         alns_params = A.AlnsParams(max_iter=10)
         if fit_cooling:  # calibration stretch: iteration time of this pool on this instance
@@ -129,7 +134,10 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_
                 trace.append((time.perf_counter() - t0, best[0]))
             return time.perf_counter() >= alns_end
 
-        A._DeviceWorkers(instance, alns_params, workers).drive(stop=stop, max_stretch=25)
+        # stretches of <= ~2 s so that the stage ends near its deadline (an
+        # iteration takes ~0.5 s per worker at n = 999)
+        stretch = 25 if per_iter is None else max(1, min(25, int(2.0 / max(per_iter, 1e-6))))
+        A._DeviceWorkers(instance, alns_params, workers).drive(stop=stop, max_stretch=stretch)
     if time.perf_counter() < final_start:
         rng = R.philox_generator(A.worker_seed(seed, 7001), R.BRKGA_STREAM)
         pop = B.warm_start_population_device(instance, best[1], brkga_params, rng)
