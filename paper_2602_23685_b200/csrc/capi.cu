@@ -21,6 +21,9 @@ struct vrp_instance {
 namespace {
 thread_local char g_err[512] = "";
 
+__global__ void probe_kernel() {}
+const void *probe_kernel_ptr() { return reinterpret_cast<const void *>(&probe_kernel); }
+
 int fail(int code, const char *fmt, const char *arg = "") {
     snprintf(g_err, sizeof(g_err), fmt, arg);
     return code;
@@ -30,6 +33,21 @@ int cuda_fail(cudaError_t e, const char *where) {
     snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
     return VRP_ECUDA;
 }
+
+// Every handle-taking entry point runs on the handle's device (the calling
+// thread's current device is restored on return), so one process can drive
+// several GPUs with one instance handle per device.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
 
 int launch_result(int rc, const char *what) {
     if (rc == 0) return 0;
@@ -44,7 +62,11 @@ extern "C" {
 
 int vrp_version(int32_t *abi_version, int32_t *compiled_arch) {
     if (abi_version) *abi_version = 1;
-    if (compiled_arch) *compiled_arch = 1000;
+    if (compiled_arch) {
+        // the SASS architecture of this library's kernels (100 = sm_100a), times 10
+        cudaFuncAttributes fa;
+        *compiled_arch = cudaFuncGetAttributes(&fa, probe_kernel_ptr()) == cudaSuccess ? fa.binaryVersion * 10 : 1000;
+    }
     return 0;
 }
 
@@ -126,6 +148,7 @@ int vrp_instance_destroy(vrp_instance_t h) {
 
 int vrp_instance_info(vrp_instance_t h, int32_t *n, int32_t *m, int32_t *k, int32_t *integral) {
     if (!h) return fail(VRP_EINVAL, "null instance%s");
+    DeviceGuard dg(h->device);
     if (n) *n = h->dev.n;
     if (m) *m = h->dev.m;
     if (k) *k = h->dev.k;
@@ -137,6 +160,7 @@ int vrp_makespan_batch(vrp_instance_t h, const void *ops, int32_t op_bytes, int6
                        const int32_t *lens, int64_t N, int32_t mode, double *z, int32_t *status,
                        double *returns, int32_t *bottleneck, void *stream) {
     if (!h) return fail(VRP_EINVAL, "null instance%s");
+    DeviceGuard dg(h->device);
     if (N < 0 || (N > 0 && (!ops || !lens || !z || !status)))
         return fail(VRP_EINVAL, "vrp_makespan_batch: null buffer%s");
     if (op_bytes != 2 && op_bytes != 4) return fail(VRP_EINVAL, "op_bytes must be 2 or 4%s");
@@ -152,6 +176,7 @@ int vrp_evaluate_records(vrp_instance_t h, const int32_t *ops, int64_t op_stride
                          int64_t N, double *z, int32_t *status, double *returns, double *arrival,
                          double *time, int32_t *q0, void *stream) {
     if (!h) return fail(VRP_EINVAL, "null instance%s");
+    DeviceGuard dg(h->device);
     if (N < 0 || (N > 0 && (!ops || !lens || !z || !status || !arrival || !time)))
         return fail(VRP_EINVAL, "vrp_evaluate_records: null buffer%s");
     if (N == 0) return 0;
@@ -165,6 +190,7 @@ int vrp_decode_batch(vrp_instance_t h, const double *genes, int64_t gene_stride,
                      int32_t *scheduled, int64_t *visits, void *ops_out, int32_t op_bytes,
                      int64_t out_stride, int32_t *lens_out, void *stream) {
     if (!h) return fail(VRP_EINVAL, "null instance%s");
+    DeviceGuard dg(h->device);
     if (N < 0 || (N > 0 && (!genes || !fitness))) return fail(VRP_EINVAL, "vrp_decode_batch: null buffer%s");
     if (ops_out && op_bytes != 2 && op_bytes != 4) return fail(VRP_EINVAL, "op_bytes must be 2 or 4%s");
     if (ops_out && out_stride < 2 * (int64_t)h->dev.n) return fail(VRP_EINVAL, "out_stride < 2n%s");
@@ -217,6 +243,7 @@ int vrp_repair_batch(vrp_instance_t h, const int32_t *partial_ops, int64_t parti
                      int32_t *out_ops, int64_t out_stride, int32_t *out_lens, int32_t *status,
                      int64_t N, void *stream) {
     if (!h) return fail(VRP_EINVAL, "null instance%s");
+    DeviceGuard dg(h->device);
     if (N < 0 || (N > 0 && (!partial_ops || !partial_lens || !removed || !nremoved || !regret_k ||
                             !out_ops || !out_lens || !status)))
         return fail(VRP_EINVAL, "vrp_repair_batch: null buffer%s");
@@ -234,6 +261,7 @@ int vrp_alns_iterate(vrp_instance_t h, const vrp_alns_params *params, vrp_alns_w
                      int64_t it_end, int32_t *trace_it, double *trace_z, int64_t trace_cap,
                      int32_t *rows_it, double *rows_val, int64_t rows_cap, void *stream) {
     if (!h) return fail(VRP_EINVAL, "null instance%s");
+    DeviceGuard dg(h->device);
     if (!params) return fail(VRP_EINVAL, "vrp_alns_iterate: null params%s");
     if (nw < 0 || it_begin < 1) return fail(VRP_EINVAL, "vrp_alns_iterate: bad worker count / iteration%s");
     if (nw == 0 || it_end < it_begin) return 0;
@@ -253,6 +281,7 @@ int vrp_destroy_batch(vrp_instance_t h, const int32_t *ops, int64_t op_stride, c
                       int32_t *out_ops, int64_t out_stride, int32_t *out_lens, int32_t *removed,
                       int64_t removed_stride, int32_t *nremoved, int64_t N, void *stream) {
     if (!h) return fail(VRP_EINVAL, "null instance%s");
+    DeviceGuard dg(h->device);
     if (N < 0) return fail(VRP_EINVAL, "vrp_destroy_batch: N < 0%s");
     if (N == 0) return 0;
     if (!ops || !lens || !opcode || !q || !states || !out_ops || !out_lens || !removed || !nremoved)
@@ -271,6 +300,7 @@ int vrp_remove_batch(vrp_instance_t h, const int32_t *ops, int64_t op_stride, co
                      int64_t out_stride, int32_t *out_lens, int32_t *removed, int64_t removed_stride,
                      int32_t *nremoved, int64_t N, void *stream) {
     if (!h) return fail(VRP_EINVAL, "null instance%s");
+    DeviceGuard dg(h->device);
     if (N < 0) return fail(VRP_EINVAL, "vrp_remove_batch: N < 0%s");
     if (N == 0) return 0;
     if (!ops || !lens || !picked || !npicked || !out_ops || !out_lens || !removed || !nremoved)
@@ -287,6 +317,7 @@ int vrp_remove_batch(vrp_instance_t h, const int32_t *ops, int64_t op_stride, co
 int vrp_removal_gains(vrp_instance_t h, const int32_t *ops, int64_t op_stride, const int32_t *lens,
                       double *gains, int64_t gains_stride, int64_t N, void *stream) {
     if (!h) return fail(VRP_EINVAL, "null instance%s");
+    DeviceGuard dg(h->device);
     if (N < 0) return fail(VRP_EINVAL, "vrp_removal_gains: N < 0%s");
     if (N == 0) return 0;
     if (!ops || !lens || !gains) return fail(VRP_EINVAL, "vrp_removal_gains: null buffer%s");
@@ -308,6 +339,7 @@ int vrp_ls_build(vrp_instance_t h, int32_t kind, const int32_t *base_ops, const 
                  const int64_t *index_list, int64_t first, int64_t count, void *out_ops,
                  int32_t op_bytes, int32_t *out_lens, void *stream) {
     if (!h) return fail(VRP_EINVAL, "null instance%s");
+    DeviceGuard dg(h->device);
     if (kind < 0 || kind > 3) return fail(VRP_EINVAL, "vrp_ls_build: kind must lie in 0..3%s");
     if (op_bytes != 2 && op_bytes != 4) return fail(VRP_EINVAL, "vrp_ls_build: op_bytes must be 2 or 4%s");
     if (count < 0 || n_entries < 0) return fail(VRP_EINVAL, "vrp_ls_build: negative count%s");

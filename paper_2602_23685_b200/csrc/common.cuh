@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #define VRP_FULL_MASK 0xffffffffu
 
 // Device view of an uploaded instance (instance.py:82-156).
@@ -60,4 +62,33 @@ struct LaunchShape {
     int warps_per_block;
     int blocks;
     size_t smem_bytes;
+};
+
+// Launch plans (block shape, dynamic shared memory, the MaxDynamicSharedMemory
+// attribute) computed once per (device, key) and kept per device -- the
+// attribute is per device -- under a mutex, so one process may drive several
+// GPUs from several threads.  make(plan) returns 0 or an error code.
+constexpr int VRP_MAX_DEVICES = 64;
+template <typename Plan>
+struct PlanCache {
+    std::mutex mu;
+    int64_t key[VRP_MAX_DEVICES];
+    bool valid[VRP_MAX_DEVICES] = {};
+    Plan plan[VRP_MAX_DEVICES];
+
+    template <typename F>
+    int get(int64_t k, Plan &out, F make) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= VRP_MAX_DEVICES) return -1;
+        std::lock_guard<std::mutex> lock(mu);
+        if (!valid[dev] || key[dev] != k) {
+            valid[dev] = false;
+            const int rc = make(plan[dev]);
+            if (rc) return rc;
+            key[dev] = k;
+            valid[dev] = true;
+        }
+        out = plan[dev];
+        return 0;
+    }
 };

@@ -715,6 +715,31 @@ decode_multi_kernel(DevInstance I, const double *__restrict__ genes, int64_t gst
     }
 }
 
+// (warps per block, resident blocks) maximising resident warps per SM for a
+// dynamic shared-memory footprint of per_warp bytes per warp
+struct DecodePlan {
+    int w, blocks;
+};
+
+template <typename Kern>
+int plan_decode(Kern kern, size_t per_warp, DecodePlan &out) {
+    int best_w = 0, best_res = 0, best_blocks = 0;
+    for (int w = 8; w >= 1; --w) {
+        const size_t bytes = per_warp * (size_t)w;
+        if (bytes > 227 * 1024) continue;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+            return -1;
+        int blocks = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32 * w, bytes) != cudaSuccess) return -1;
+        if (blocks * w > best_res) { best_res = blocks * w; best_w = w; best_blocks = blocks; }
+    }
+    if (!best_res) return -2;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per_warp * best_w)) != cudaSuccess)
+        return -1;
+    out = DecodePlan{best_w, best_blocks};
+    return 0;
+}
+
 template <bool INTD, typename OutT, bool NARROW, int P, int MC = 0>
 int launch_m(const DevInstance &I, const double *genes, int64_t gstride, int64_t N, int relax,
              double penalty, double *fitness, double *makespan, int32_t *scheduled, int64_t *visits,
@@ -723,24 +748,11 @@ int launch_m(const DevInstance &I, const double *genes, int64_t gstride, int64_t
     constexpr int G = 32 / P;
     auto kern = decode_multi_kernel<INTD, OutT, NARROW, P, MC>;
     const size_t per_warp = multi_layout(I.n, NARROW ? 4 : 8).total * G;
-    static size_t cached_pw = 0;
-    static int cached_w = 0, cached_blocks = 0;
-    if (cached_pw != per_warp) {
-        int best_w = 0, best_res = 0, best_blocks = 0;
-        for (int w = 8; w >= 1; --w) {
-            size_t bytes = per_warp * (size_t)w;
-            if (bytes > 227 * 1024) continue;
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
-                return -1;
-            int blocks = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32 * w, bytes) != cudaSuccess)
-                return -1;
-            if (blocks * w > best_res) { best_res = blocks * w; best_w = w; best_blocks = blocks; }
-        }
-        if (!best_res) return -2;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per_warp * best_w));
-        cached_pw = per_warp; cached_w = best_w; cached_blocks = best_blocks;
-    }
+    static PlanCache<DecodePlan> cache;
+    DecodePlan pl;
+    const int rc = cache.get((int64_t)per_warp, pl, [&](DecodePlan &out) { return plan_decode(kern, per_warp, out); });
+    if (rc) return rc;
+    const int cached_w = pl.w, cached_blocks = pl.blocks;
     const size_t bytes = per_warp * (size_t)cached_w;
     const int64_t nwarps = (N + G - 1) / G;
     int64_t want = (nwarps + cached_w - 1) / cached_w;
@@ -762,24 +774,11 @@ int launch_k(const DevInstance &I, const double *genes, int64_t gstride, int64_t
              uint8_t *retry, const uint8_t *only, cudaStream_t stream, int sm_count) {
     auto kern = decode_kernel<INTD, OutT, NARROW, MC>;
     const size_t per_warp = decode_layout(I.n, NARROW ? 4 : 8).total;
-    static size_t cached_pw = 0;
-    static int cached_w = 0, cached_blocks = 0;
-    if (cached_pw != per_warp) {
-        int best_w = 0, best_res = 0, best_blocks = 0;
-        for (int w = 8; w >= 1; --w) {
-            size_t bytes = per_warp * (size_t)w;
-            if (bytes > 227 * 1024) continue;
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
-                return -1;
-            int blocks = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32 * w, bytes) != cudaSuccess)
-                return -1;
-            if (blocks * w > best_res) { best_res = blocks * w; best_w = w; best_blocks = blocks; }
-        }
-        if (!best_res) return -2;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per_warp * best_w));
-        cached_pw = per_warp; cached_w = best_w; cached_blocks = best_blocks;
-    }
+    static PlanCache<DecodePlan> cache;
+    DecodePlan pl;
+    const int rc = cache.get((int64_t)per_warp, pl, [&](DecodePlan &out) { return plan_decode(kern, per_warp, out); });
+    if (rc) return rc;
+    const int cached_w = pl.w, cached_blocks = pl.blocks;
     const size_t bytes = per_warp * (size_t)cached_w;
     int64_t want = (N + cached_w - 1) / cached_w;
     int64_t grid = (int64_t)cached_blocks * sm_count;
@@ -838,39 +837,49 @@ int launch_t(const DevInstance &I, const double *genes, int64_t gstride, int64_t
     const int two_n = 2 * I.n;
     uint16_t *order = nullptr;
     uint32_t *seq = nullptr;
-    uint8_t *retry = nullptr;
-    if (cudaMallocAsync(&order, sizeof(uint16_t) * (size_t)N * two_n, stream) != cudaSuccess) return -1;
-    if (ops_out && cudaMallocAsync(&seq, sizeof(uint32_t) * (size_t)N * two_n, stream) != cudaSuccess) return -1;
+    uint8_t *retry = nullptr, *fb = nullptr;
+    auto release = [&]() {  // every exit path frees the scratch
+        if (order) cudaFreeAsync(order, stream);
+        if (fb) cudaFreeAsync(fb, stream);
+        if (seq) cudaFreeAsync(seq, stream);
+        if (retry) cudaFreeAsync(retry, stream);
+    };
+    // the sort kernels' shared memory per warp; as many warps per block as fit
+    const size_t bper = bucket_sort_bytes(I.n), sper = sort_bytes(I.n);
+    if (bper > 227 * 1024 || sper > 227 * 1024) return -2;  // n beyond the sort's shared-memory footprint
     // narrow tables where shared memory limits residency (measured: a280
     // +25 % with the segmented kernel; below n ~ 200 registers bound it)
     const char *nm = getenv("VRP_DECODE_NARROW_MIN");  // (ablation knob)
     const bool narrow = INTD && I.n >= (nm ? atoi(nm) : 200);
-    if (narrow && cudaMallocAsync(&retry, (size_t)N, stream) != cudaSuccess) return -1;
-    uint8_t *fb = nullptr;
-    if (cudaMallocAsync(&fb, (size_t)N, stream) != cudaSuccess) return -1;
+    if (cudaMallocAsync(&order, sizeof(uint16_t) * (size_t)N * two_n, stream) != cudaSuccess ||
+        (ops_out && cudaMallocAsync(&seq, sizeof(uint32_t) * (size_t)N * two_n, stream) != cudaSuccess) ||
+        (narrow && cudaMallocAsync(&retry, (size_t)N, stream) != cudaSuccess) ||
+        cudaMallocAsync(&fb, (size_t)N, stream) != cudaSuccess) {
+        release();
+        return -1;
+    }
     {
-        const int sw = 4;
-        static int bucket_n = -1, sort_n = -1;
-        const size_t bbytes = bucket_sort_bytes(I.n) * sw, sbytes = sort_bytes(I.n) * sw;
-        if (bucket_n != I.n) {
-            if (cudaFuncSetAttribute(bucket_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bbytes) != cudaSuccess)
+        auto fit = [](size_t per) { int w = 4; while (w > 1 && per * w > 227 * 1024) --w; return w; };
+        const int bw = fit(bper), sw = fit(sper);
+        const size_t bbytes = bper * bw, sbytes = sper * sw;
+        struct SortPlan { int bblocks, sblocks; };
+        static PlanCache<SortPlan> cache;
+        SortPlan sp;
+        const int rc0 = cache.get(I.n, sp, [&](SortPlan &out) {
+            if (cudaFuncSetAttribute(bucket_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bbytes) != cudaSuccess ||
+                cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbytes) != cudaSuccess)
                 return -1;
-            bucket_n = I.n;
-        }
-        if (sort_n != I.n) {
-            if (cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbytes) != cudaSuccess)
-                return -1;
-            sort_n = I.n;
-        }
-        const int64_t swant = (N + sw - 1) / sw;
-        int bblocks = 0, sblocks = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bblocks, bucket_sort_kernel, 32 * sw, bbytes);
-        int64_t bgrid = (int64_t)(bblocks > 0 ? bblocks : 1) * sm_count;
-        if (bgrid > swant) bgrid = swant;
-        bucket_sort_kernel<<<(unsigned)bgrid, 32 * sw, bbytes, stream>>>(genes, gstride, N, two_n, order, fb);
+            out.bblocks = out.sblocks = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&out.bblocks, bucket_sort_kernel, 32 * bw, bbytes);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&out.sblocks, sort_kernel, 32 * sw, sbytes);
+            return 0;
+        });
+        if (rc0) { release(); return rc0; }
+        int64_t bgrid = (int64_t)(sp.bblocks > 0 ? sp.bblocks : 1) * sm_count, bwant = (N + bw - 1) / bw;
+        if (bgrid > bwant) bgrid = bwant;
+        bucket_sort_kernel<<<(unsigned)bgrid, 32 * bw, bbytes, stream>>>(genes, gstride, N, two_n, order, fb);
         // the (normally few) chromosomes whose priorities cluster: bitonic network
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sblocks, sort_kernel, 32 * sw, sbytes);
-        int64_t sgrid = (int64_t)(sblocks > 0 ? sblocks : 1) * sm_count;
+        int64_t sgrid = (int64_t)(sp.sblocks > 0 ? sp.sblocks : 1) * sm_count, swant = (N + sw - 1) / sw;
         if (sgrid > swant) sgrid = swant;
         sort_kernel<<<(unsigned)sgrid, 32 * sw, sbytes, stream>>>(genes, gstride, N, two_n, order, fb);
     }
@@ -888,10 +897,7 @@ int launch_t(const DevInstance &I, const double *genes, int64_t gstride, int64_t
                                          visits, ops_out, ostride, lens_out, order, seq, nullptr, nullptr,
                                          stream, sm_count);
     }
-    cudaFreeAsync(order, stream);
-    cudaFreeAsync(fb, stream);
-    if (seq) cudaFreeAsync(seq, stream);
-    if (retry) cudaFreeAsync(retry, stream);
+    release();
     return rc;
 }
 

@@ -562,15 +562,13 @@ int launch_t(const DevInstance &I, const void *ops, int64_t stride, const int32_
              double *arrival, double *timev, int32_t *q0, cudaStream_t stream, int sm_count,
              int fixup) {
     auto kern = makespan_kernel<OpT, INTD, MODE, REC, NARROW, COMPACT, MC, RA>;
-    static int cached_n = -1, cached_m = -1;
-    static Shape sh;
-    if (cached_n != I.n || cached_m != I.m) {
+    static PlanCache<Shape> cache;  // per instantiation, per device
+    Shape sh;
+    const int rc = cache.get(((int64_t)I.n << 8) | I.m, sh, [&](Shape &out) {
         using RT = typename std::conditional<NARROW, uint32_t, TimeT<INTD>>::type;
-        const int rc = plan(kern, I.n, I.m, MODE, (int)sizeof(RT), COMPACT, sh);
-        if (rc) return rc;
-        cached_n = I.n;
-        cached_m = I.m;
-    }
+        return plan(kern, I.n, I.m, MODE, (int)sizeof(RT), COMPACT, out);
+    });
+    if (rc) return rc;
     const int64_t per_block = (int64_t)sh.wpb * sh.G;
     const int64_t want = (N + per_block - 1) / per_block;
     int64_t grid = (int64_t)sh.blocks * sm_count;

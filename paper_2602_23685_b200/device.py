@@ -72,6 +72,18 @@ def device_instance(instance) -> DeviceInstance:
     return di
 
 
+def _check_out(res, dev, **spec):
+    """Caller-supplied output tensors must match the batch (the kernels write
+    through their raw pointers)."""
+    for name, (shape, dtype) in spec.items():
+        t = res.get(name)
+        if t is None:
+            continue
+        if tuple(t.shape) != tuple(shape) or t.dtype != dtype or t.device != dev or not t.is_contiguous():
+            raise ValueError(f"out[{name!r}] must be a contiguous {dtype} tensor of shape {tuple(shape)} on {dev}, "
+                             f"got {t.dtype} {tuple(t.shape)} on {t.device}")
+
+
 def row_stride(t) -> int:
     """Elements between rows; a size-1 leading dim may report any stride."""
     return int(t.stride(0)) if t.shape[0] > 1 else int(t.shape[1])
@@ -114,6 +126,8 @@ def makespan_batch(instance, ops, lens, mode: int = N.MODE_EXACT, want_returns: 
         res["returns"] = torch.empty((Nc, di.m), dtype=torch.float64, device=dev)
     if want_bottleneck and "bottleneck" not in res:
         res["bottleneck"] = torch.empty(Nc, dtype=torch.int32, device=dev)
+    _check_out(res, dev, z=((Nc,), torch.float64), status=((Nc,), torch.int32),
+               returns=((Nc, di.m), torch.float64), bottleneck=((Nc,), torch.int32))
     L = N.lib()
     N.check(L.vrp_makespan_batch(di.handle, N.ptr(ops), ops.element_size(), row_stride(ops),
                                  N.ptr(lens), Nc, int(mode), N.ptr(res["z"]), N.ptr(res["status"]),
@@ -168,6 +182,13 @@ def decode_batch(instance, genes, relax: bool = True, penalty: float = 1e6,
     if want_solution and "ops" not in res:
         res["ops"] = torch.empty((Nc, 2 * di.n), dtype=op_dtype, device=dev)
         res["lens"] = torch.empty((Nc, di.m), dtype=torch.int32, device=dev)
+    _check_out(res, dev, fitness=((Nc,), torch.float64), makespan=((Nc,), torch.float64),
+               scheduled=((Nc,), torch.int32), visits=((Nc,), torch.int64), lens=((Nc, di.m), torch.int32))
+    if want_solution:
+        o = res["ops"]
+        if o.dim() != 2 or o.shape[0] != Nc or o.shape[1] < 2 * di.n or o.dtype not in (torch.int16, torch.int32) \
+                or o.device != dev:
+            raise ValueError(f"out['ops'] must be int16/int32 [N={Nc}, >=2n] on {dev}")
     ops = res.get("ops") if want_solution else None
     N.check(N.lib().vrp_decode_batch(
         di.handle, N.ptr(genes), row_stride(genes), Nc, int(bool(relax)), float(penalty),
@@ -179,12 +200,12 @@ def decode_batch(instance, genes, relax: bool = True, penalty: float = 1e6,
     return res
 
 
-_PIPE = {}
-
-
 def _pipeline(di, chunk: int, op_dtype):
-    key = (id(di), torch.cuda.current_device(), chunk, op_dtype)
-    st = _PIPE.get(key)
+    # held by the DeviceInstance (one device each), so the buffers live exactly
+    # as long as the instance
+    pipes = di.__dict__.setdefault("_pipes", {})
+    key = (chunk, op_dtype)
+    st = pipes.get(key)
     if st is None:
         dev = torch.device("cuda", torch.cuda.current_device())
         st = {"streams": [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)],
@@ -193,7 +214,7 @@ def _pipeline(di, chunk: int, op_dtype):
                         "z": torch.empty(chunk, dtype=torch.float64, device=dev),
                         "status": torch.empty(chunk, dtype=torch.int32, device=dev)}
                        for _ in range(2)]}
-        _PIPE[key] = st
+        pipes[key] = st
     return st
 
 
