@@ -210,6 +210,22 @@ int vrp_ls_build(vrp_instance_t h, int32_t kind, const int32_t *base_ops, const 
  * x, y: n DEVICE doubles. */
 int vrp_sa_exp(const double *x, double *y, int64_t n, void *stream);
 
+/* The verification shortlist of the batched local search (alns.py:401-413:
+ * stable sort of the survivors by estimate, first _VERIFY_LIMIT), per solution,
+ * over a chunk of estimated candidates: candidates with status 0 and
+ * z < zthr[worker] are merged into each solution's running list of its K
+ * smallest (estimate, generation index) pairs (K <= 16).
+ *   z/status[count]            K2 output for candidates first .. first+count-1 (DEVICE)
+ *   seg_worker/seg_begin/seg_end[nseg]  host-planned segments of <= 2048
+ *                              candidates of one solution each (global indices)
+ *   workers/wseg_first/wseg_count[nworkers]  solutions with segments in this
+ *                              chunk and their segment ranges
+ *   top_z/top_i[W][K], top_n[W] running lists, sorted (DEVICE, in/out) */
+int vrp_ls_topk(const double *z, const int32_t *status, int64_t first, const double *zthr,
+                const int32_t *seg_worker, const int64_t *seg_begin, const int64_t *seg_end, int64_t nseg,
+                const int32_t *workers, const int32_t *wseg_first, const int32_t *wseg_count, int32_t nworkers,
+                int32_t K, double *top_z, int64_t *top_i, int32_t *top_n, void *stream);
+
 /* One ALNS worker (alns.py:536-640 run_alns locals), DEVICE-resident.
  * weights/scores/attempts are indexed in the reference's operator order:
  * random, worst, shaw, cluster, route, critical_path, greedy, regret2,

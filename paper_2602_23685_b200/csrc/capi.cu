@@ -355,6 +355,22 @@ int vrp_ls_build(vrp_instance_t h, int32_t kind, const int32_t *base_ops, const 
                          "vrp_ls_build");
 }
 
+int vrp_ls_topk(const double *z, const int32_t *status, int64_t first, const double *zthr,
+                const int32_t *seg_worker, const int64_t *seg_begin, const int64_t *seg_end, int64_t nseg,
+                const int32_t *workers, const int32_t *wseg_first, const int32_t *wseg_count, int32_t nworkers,
+                int32_t K, double *top_z, int64_t *top_i, int32_t *top_n, void *stream) {
+    if (nseg < 0 || nworkers < 0) return fail(VRP_EINVAL, "vrp_ls_topk: negative count%s");
+    if (K < 1 || K > 16) return fail(VRP_EINVAL, "vrp_ls_topk: K must lie in 1..16%s");
+    if (nseg == 0 || nworkers == 0) return 0;
+    if (!z || !status || !zthr || !seg_worker || !seg_begin || !seg_end || !workers || !wseg_first || !wseg_count ||
+        !top_z || !top_i || !top_n)
+        return fail(VRP_EINVAL, "vrp_ls_topk: null buffer%s");
+    return launch_result(launch_ls_topk(z, status, first, zthr, seg_worker, seg_begin, seg_end, nseg, workers,
+                                        wseg_first, wseg_count, nworkers, K, top_z, top_i, top_n,
+                                        static_cast<cudaStream_t>(stream)),
+                         "vrp_ls_topk");
+}
+
 int vrp_random_fill(vrp_philox *state, int64_t count, double *out, void *stream) {
     if (count < 0) return fail(VRP_EINVAL, "vrp_random_fill: count < 0%s");
     if (count == 0) return 0;

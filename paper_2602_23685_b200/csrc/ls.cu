@@ -147,6 +147,115 @@ ls_build_kernel(int kind, int n, int m, const int32_t *__restrict__ base_ops, co
     }
 }
 
+// ---- per-solution top-K of the local-search survivors (alns.py:401-413: the
+// stable sort by estimate + [:_VERIFY_LIMIT] over candidates in generation
+// order == the K smallest (estimate, generation index) pairs)
+constexpr int LS_SEG = 2048;  // candidates per segment (one worker each)
+
+__device__ __forceinline__ bool zi_lt(double za, int64_t ia, double zb, int64_t ib) {
+    return za < zb || (za == zb && ia < ib);
+}
+
+// segment s: the K smallest survivors (status 0, z < zthr[worker]) of
+// candidates [seg_begin, seg_end) -- K rounds of block argmin above the last pick
+__global__ void __launch_bounds__(256)
+ls_seg_topk_kernel(const double *__restrict__ z, const int32_t *__restrict__ status, int64_t first,
+                   const double *__restrict__ zthr, const int32_t *__restrict__ seg_worker,
+                   const int64_t *__restrict__ seg_begin, const int64_t *__restrict__ seg_end, int K,
+                   double *__restrict__ out_z, int64_t *__restrict__ out_i, int32_t *__restrict__ out_n) {
+    __shared__ double sz[8];
+    __shared__ int64_t si[8];
+    constexpr int PER = LS_SEG / 256;
+    const int s = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t b = seg_begin[s], e = seg_end[s];
+    const double thr = zthr[seg_worker[s]];
+    double vz[PER];
+    int64_t vi[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int64_t g = b + threadIdx.x + 256 * k;
+        const bool ok = g < e && status[g - first] == 0 && z[g - first] < thr;
+        vz[k] = ok ? z[g - first] : INFINITY;
+        vi[k] = ok ? g : INT64_MAX;
+    }
+    double lz = -INFINITY;
+    int64_t li = -1;
+    int cnt = 0;
+    for (int r = 0; r < K; ++r) {
+        double bz = INFINITY;
+        int64_t bi = INT64_MAX;
+#pragma unroll
+        for (int k = 0; k < PER; ++k)
+            if (vi[k] != INT64_MAX && zi_lt(lz, li, vz[k], vi[k]) && zi_lt(vz[k], vi[k], bz, bi)) { bz = vz[k]; bi = vi[k]; }
+        for (int o = 16; o; o >>= 1) {
+            const double oz = __shfl_xor_sync(VRP_FULL_MASK, bz, o);
+            const int64_t oi = __shfl_xor_sync(VRP_FULL_MASK, bi, o);
+            if (zi_lt(oz, oi, bz, bi)) { bz = oz; bi = oi; }
+        }
+        if (lane == 0) { sz[warp] = bz; si[warp] = bi; }
+        __syncthreads();
+        bz = INFINITY; bi = INT64_MAX;
+        for (int w = 0; w < 8; ++w)
+            if (zi_lt(sz[w], si[w], bz, bi)) { bz = sz[w]; bi = si[w]; }
+        __syncthreads();
+        if (bi == INT64_MAX) break;
+        if (threadIdx.x == 0) { out_z[(int64_t)s * K + r] = bz; out_i[(int64_t)s * K + r] = bi; }
+        lz = bz; li = bi;
+        ++cnt;
+    }
+    if (threadIdx.x == 0) out_n[s] = cnt;
+}
+
+// worker w: merge its running list with its segments' lists (warp per worker)
+__global__ void __launch_bounds__(32)
+ls_merge_topk_kernel(const int32_t *__restrict__ workers, const int32_t *__restrict__ wseg_first,
+                     const int32_t *__restrict__ wseg_count, int K, const double *__restrict__ seg_z,
+                     const int64_t *__restrict__ seg_i, const int32_t *__restrict__ seg_n,
+                     double *__restrict__ top_z, int64_t *__restrict__ top_i, int32_t *__restrict__ top_n) {
+    const int lane = threadIdx.x;
+    const int w = workers[blockIdx.x];
+    const int s0 = wseg_first[blockIdx.x], ns = wseg_count[blockIdx.x];
+    const int tot = (ns + 1) * K;  // slot j < K: running list; then K per segment
+    auto at = [&](int j, double &zz, int64_t &ii) -> bool {
+        const int src = j / K, r = j - src * K;
+        if (src == 0) {
+            if (r >= top_n[w]) return false;
+            zz = top_z[(int64_t)w * K + r]; ii = top_i[(int64_t)w * K + r];
+            return true;
+        }
+        const int s = s0 + src - 1;
+        if (r >= seg_n[s]) return false;
+        zz = seg_z[(int64_t)s * K + r]; ii = seg_i[(int64_t)s * K + r];
+        return true;
+    };
+    double lz = -INFINITY, pz[16];
+    int64_t li = -1, pi[16];
+    int cnt = 0;
+    for (int r = 0; r < K; ++r) {
+        double bz = INFINITY;
+        int64_t bi = INT64_MAX;
+        for (int j = lane; j < tot; j += 32) {
+            double zz;
+            int64_t ii;
+            if (at(j, zz, ii) && zi_lt(lz, li, zz, ii) && zi_lt(zz, ii, bz, bi)) { bz = zz; bi = ii; }
+        }
+        for (int o = 16; o; o >>= 1) {
+            const double oz = __shfl_xor_sync(VRP_FULL_MASK, bz, o);
+            const int64_t oi = __shfl_xor_sync(VRP_FULL_MASK, bi, o);
+            if (zi_lt(oz, oi, bz, bi)) { bz = oz; bi = oi; }
+        }
+        if (bi == INT64_MAX) break;
+        pz[r] = bz; pi[r] = bi;
+        lz = bz; li = bi;
+        ++cnt;
+    }
+    __syncwarp();  // every lane has read the running list before lane 0 rewrites it
+    if (lane == 0) {
+        for (int r = 0; r < cnt; ++r) { top_z[(int64_t)w * K + r] = pz[r]; top_i[(int64_t)w * K + r] = pi[r]; }
+        top_n[w] = cnt;
+    }
+}
+
 }  // namespace
 
 int launch_ls_build(int kind, int n, int m, const int32_t *base_ops, const int32_t *base_lens,
@@ -165,4 +274,30 @@ int launch_ls_build(int kind, int n, int m, const int32_t *base_ops, const int32
             kind, n, m, base_ops, base_lens, entries, entry_start, n_entries, index_list, first, count,
             (int32_t *)out_ops, out_lens);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_ls_topk(const double *z, const int32_t *status, int64_t first, const double *zthr,
+                   const int32_t *seg_worker, const int64_t *seg_begin, const int64_t *seg_end, int64_t nseg,
+                   const int32_t *workers, const int32_t *wseg_first, const int32_t *wseg_count, int32_t nworkers,
+                   int32_t K, double *top_z, int64_t *top_i, int32_t *top_n, cudaStream_t stream) {
+    if (nseg <= 0 || nworkers <= 0) return 0;
+    double *sz = nullptr;
+    int64_t *si = nullptr;
+    int32_t *sn = nullptr;
+    if (cudaMallocAsync(&sz, sizeof(double) * (size_t)nseg * K, stream) != cudaSuccess) return -1;
+    if (cudaMallocAsync(&si, sizeof(int64_t) * (size_t)nseg * K, stream) != cudaSuccess ||
+        cudaMallocAsync(&sn, sizeof(int32_t) * (size_t)nseg, stream) != cudaSuccess) {
+        cudaFreeAsync(sz, stream);
+        if (si) cudaFreeAsync(si, stream);
+        return -1;
+    }
+    ls_seg_topk_kernel<<<(unsigned)nseg, 256, 0, stream>>>(z, status, first, zthr, seg_worker, seg_begin, seg_end, K,
+                                                           sz, si, sn);
+    ls_merge_topk_kernel<<<(unsigned)nworkers, 32, 0, stream>>>(workers, wseg_first, wseg_count, K, sz, si, sn,
+                                                                top_z, top_i, top_n);
+    const cudaError_t e = cudaPeekAtLastError();
+    cudaFreeAsync(sz, stream);
+    cudaFreeAsync(si, stream);
+    cudaFreeAsync(sn, stream);
+    return e == cudaSuccess ? 0 : -1;
 }

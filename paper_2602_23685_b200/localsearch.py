@@ -10,7 +10,8 @@ Each improvement pass of every solution is:
      ``two_pass_estimate`` -- nothing is materialised on the host;
   3. survivors (status 0, estimate < z - 1e-9) reduced on the device to each
      solution's ten best by (estimate, generation index) -- the reference's
-     stable sort + ``[:_VERIFY_LIMIT]``;
+     stable sort + ``[:_VERIFY_LIMIT]`` -- by ``vrp_ls_topk`` (per-segment
+     block top-10, then a per-solution merge with the running list);
   4. those ten re-built and scored by K1 ``exact_makespan``; the first strictly
      best improvement (< z - 1e-9) replaces the solution (alns.py:401-413).
 A solution leaves the loop when a pass finds nothing, exactly like the
@@ -42,50 +43,70 @@ def _build(instance, kind, ops_t, lens_t, ent_t, start_t, first, count, index_li
     return out, olen
 
 
+SEG = 2048  # candidates per top-K segment (csrc/ls.cu LS_SEG)
+
+
+def _segments(wid, wb, we, first, cnt):
+    """Segments of <= SEG candidates of one solution each covering the chunk
+    [first, first + cnt) (solutions' candidate ranges [wb, we) are disjoint
+    and ascending).  Returns the vrp_ls_topk tables (numpy)."""
+    lo = np.maximum(wb, first)
+    hi = np.minimum(we, first + cnt)
+    live = np.flatnonzero(hi > lo)
+    lo, hi, wid = lo[live], hi[live], wid[live]
+    nseg = (hi - lo + SEG - 1) // SEG
+    seg_w = np.repeat(wid, nseg).astype(np.int32)
+    k = np.arange(int(nseg.sum())) - np.repeat(np.cumsum(nseg) - nseg, nseg)
+    seg_b = np.repeat(lo, nseg) + SEG * k
+    seg_e = np.minimum(seg_b + SEG, np.repeat(hi, nseg))
+    wfirst = (np.cumsum(nseg) - nseg).astype(np.int32)
+    return seg_w, seg_b.astype(np.int64), seg_e.astype(np.int64), wid.astype(np.int32), wfirst, nseg.astype(np.int32)
+
+
 def _search(instance, kind, ops_t, lens_t, entries, counts, z):
     """Steps 2-4 for every worker that has entries.  Returns
     {worker: (z_exact, ops row, lens row)} for the workers that improved."""
     dev = ops_t.device
     n = instance.n
+    W = ops_t.shape[0]
     starts = np.zeros(len(counts), np.int64)
     np.cumsum(counts[:-1], out=starts[1:])
     total = int(counts.sum())
     ent_t = torch.from_numpy(np.ascontiguousarray(entries, np.int32)).to(dev)
     start_t = torch.from_numpy(starts).to(dev)
-    worker_t = ent_t[:, 0].long()
     zthr = torch.from_numpy(np.asarray(z, np.float64) - 1e-9).to(dev)
+    # each solution's candidates are one contiguous range (entries are grouped by solution)
+    ew = np.asarray(entries, np.int64)[:, 0]
+    wid, pos = np.unique(ew, return_index=True)
+    last = np.r_[pos[1:], ew.size] - 1
+    wb, we = starts[pos], starts[last] + counts[last]
+    # running lists: only the first top_n entries are ever read (no fill kernels)
+    top_z = torch.empty((W, VERIFY_LIMIT), dtype=torch.float64, device=dev)
+    top_i = torch.empty((W, VERIFY_LIMIT), dtype=torch.int64, device=dev)
+    top_n = torch.from_numpy(np.zeros(W, np.int32)).to(dev)
     chunk = max(1, CHUNK_BYTES // (4 * n))
-    top_w = torch.empty(0, dtype=torch.long, device=dev)
-    top_e = torch.empty(0, dtype=torch.float64, device=dev)
-    top_i = torch.empty(0, dtype=torch.long, device=dev)
     for first in range(0, total, chunk):
         cnt = min(chunk, total - first)
         c_ops, c_lens = _build(instance, kind, ops_t, lens_t, ent_t, start_t, first, cnt)
         r = DV.makespan_batch(instance, c_ops, c_lens, mode=N.MODE_TWO_PASS)
-        gidx = torch.arange(first, first + cnt, device=dev)
-        wk = worker_t[torch.searchsorted(start_t, gidx, right=True) - 1]
-        ok = (r["status"] == 0) & (r["z"] < zthr[wk])
-        # running candidates first: per worker they precede this chunk in generation order
-        w_all = torch.cat([top_w, wk[ok]])
-        e_all = torch.cat([top_e, r["z"][ok]])
-        i_all = torch.cat([top_i, gidx[ok]])
-        p1 = torch.sort(e_all, stable=True).indices
-        p2 = torch.sort(w_all[p1], stable=True).indices
-        perm = p1[p2]
-        w_s = w_all[perm]
-        rank = torch.arange(w_s.numel(), device=dev) - torch.searchsorted(w_s, w_s)
-        keep = perm[rank < VERIFY_LIMIT]
-        top_w, top_e, top_i = w_all[keep], e_all[keep], i_all[keep]
-    if top_i.numel() == 0:
+        seg_w, seg_b, seg_e, ws, wf, wc = (torch.from_numpy(x).to(dev) for x in _segments(wid, wb, we, first, cnt))
+        N.check(N.lib().vrp_ls_topk(N.ptr(r["z"]), N.ptr(r["status"]), first, N.ptr(zthr), N.ptr(seg_w),
+                                    N.ptr(seg_b), N.ptr(seg_e), seg_w.numel(), N.ptr(ws), N.ptr(wf), N.ptr(wc),
+                                    ws.numel(), VERIFY_LIMIT, N.ptr(top_z), N.ptr(top_i), N.ptr(top_n),
+                                    N.stream_handle()), "vrp_ls_topk")
+    tn = top_n.cpu().numpy()
+    if not tn.any():
         return {}
-    v_ops, v_lens = _build(instance, kind, ops_t, lens_t, ent_t, start_t, 0, top_i.numel(), index_list=top_i,
-                           op_dtype=torch.int32)
+    ti = top_i.cpu().numpy()
+    sel_w = np.repeat(np.arange(W), tn)  # (worker, estimate, index) order
+    sel_i = np.concatenate([ti[w, :tn[w]] for w in range(W) if tn[w]])
+    v_ops, v_lens = _build(instance, kind, ops_t, lens_t, ent_t, start_t, 0, sel_i.size,
+                           index_list=torch.from_numpy(sel_i).to(dev), op_dtype=torch.int32)
     r = DV.makespan_batch(instance, v_ops, v_lens, mode=N.MODE_EXACT)
     zs, st = r["z"].cpu().numpy(), r["status"].cpu().numpy()
-    ws = top_w.cpu().numpy()
     best = {}
-    for j in range(ws.size):  # sorted by (worker, estimate, index)
-        w = int(ws[j])
+    for j in range(sel_w.size):
+        w = int(sel_w[j])
         if st[j] != 0 or not zs[j] < z[w] - 1e-9:
             continue
         if w not in best or zs[j] < best[w][0]:
