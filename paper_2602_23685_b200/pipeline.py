@@ -38,7 +38,7 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_
                         initial: Solution | None = None, fit_cooling: bool = True,
                         polish: bool = True, polish_share: float | None = None,
                         final_share: float | None = None,
-                        alns_max_n: int = 400):
+                        alns_max_n: int = 400, exchange=None):
     """Best makespan found within a wall-clock budget (the BASELINE metric's
     'best makespan at fixed time'; the reference has no budget).
 
@@ -68,6 +68,10 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_
     standard (restarting) polish of the incumbent, and, if it converges
     before the deadline, iterated local search (random kicks repaired by K5,
     polished) for the rest.
+    ``exchange`` (multi-GPU, run_pipeline_budget_distributed): called as
+    exchange(z, sol, more) at every stage boundary and after every kick
+    round of the tail -- the same number of times on every rank -- it returns
+    the global best (z, sol) and whether every rank wants another round.
     Returns (best Solution, best makespan, trace [(seconds, best)])."""
     from . import baselines as BL
     t0 = time.perf_counter()
@@ -86,6 +90,16 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_
             best = (z, sol)
             trace.append((time.perf_counter() - t0, z))
 
+    def share(more=True):  # adopt the global incumbent (multi-GPU); returns the ranks' consensus on `more`
+        nonlocal best
+        if exchange is None:
+            return more
+        zg, sg, go = exchange(best[0], best[1], more)
+        if zg < best[0]:
+            best = (zg, sg)
+            trace.append((time.perf_counter() - t0, zg))
+        return go
+
     if polish_share is None:
         polish_share = (0.4 if instance.n < 500 else 0.6) if instance.n >= 90 else 0.0
     if final_share is None:  # measured (profiles/r01_summary.md): the polish + kick tail
@@ -95,6 +109,7 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_
         # than the resumed variant's ~10 s one; below that both take < 1 s)
         offer(BL.two_opt_improve(instance, best[1], move_budget=10**15,
                                  deadline=min(end, t0 + polish_share * seconds)))
+    share()
     final_start = end - (final_share * seconds if polish else 0.0)
     now = time.perf_counter()
     alns_end = now + alns_share * max(0.0, final_start - now)
@@ -138,81 +153,118 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_
         # iteration takes ~0.5 s per worker at n = 999)
         stretch = 25 if per_iter is None else max(1, min(25, int(2.0 / max(per_iter, 1e-6))))
         A._DeviceWorkers(instance, alns_params, workers).drive(stop=stop, max_stretch=stretch)
+    share()
     if time.perf_counter() < final_start:
         rng = R.philox_generator(A.worker_seed(seed, 7001), R.BRKGA_STREAM)
         pop = B.warm_start_population_device(instance, best[1], brkga_params, rng)
         sol, _ = B.run_brkga(instance, brkga_params, warm_population=pop, seed=A.worker_seed(seed, 7002),
                              deadline=final_start)
         offer(sol)
+    share()
     if polish and time.perf_counter() < end:
         offer(BL.two_opt_improve(instance, best[1], move_budget=10**15, deadline=end))
-    if polish and time.perf_counter() < end - 1.0:
+    if polish:
         # time left at a local optimum: iterated local search (batched random
-        # kicks -> K5 greedy repair -> K1 -> polish of the best kick)
-        for sol in _kick_and_polish(instance, best[1], end, seed):
-            offer(sol)
+        # kicks -> K5 greedy repair -> K1 -> polish of the best kick); with
+        # several GPUs the ranks exchange their incumbent after every round,
+        # continue from the global best and stop together
+        kick = _Kicker(instance, best[1], seed)
+        while share(time.perf_counter() + 1.2 * kick.last_s < end - 0.5):
+            sol = kick.round(end)
+            if sol is not None:
+                offer(sol)
+            kick.adopt(best[0], best[1])
     return best[1], best[0], trace
 
 
-def _kick_and_polish(instance, start: Solution, deadline: float, seed: int, batch: int = 64, q: int = 5):
-    """Iterated local search for the tail of a budget: each round destroys
-    ``q`` random customers of the current solution in ``batch`` independent
-    ways (K6), greedily repairs them (K5), scores them (K1) and polishes the
-    best one (resumed first-improvement scans).  Yields every polished
-    solution that improves on the current one."""
-    import numpy as np
-    import torch
-    from . import baselines as BL
-    from . import device as DV
-    from . import insertion as INS
-    n = instance.n
-    rng = R.philox_generator(A.worker_seed(seed, 7100), R.ALNS_STREAM)
-    cur, zcur = start, evaluate(instance, start).makespan
-    dev = torch.device("cuda", torch.cuda.current_device())
-    qq = min(q if n < 500 else 2, n)  # removals cascade; large n: smaller kicks
-    kick_s = 0.0  # duration of the last kick step (repairs do not watch the clock)
-    while time.perf_counter() + 1.2 * kick_s < deadline - 0.5:
+class _Kicker:
+    """Iterated local search for the tail of a budget, one round per call:
+    destroy ``q`` random customers of the current solution in ``batch``
+    independent ways (K6), greedily repair them (K5), score them (K1) and
+    polish the best one (resumed first-improvement scans).  ``round`` returns
+    the polished solution when it improves on the current one (else None);
+    ``adopt`` hands over an external incumbent (another GPU's)."""
+
+    def __init__(self, instance, start: Solution, seed: int, batch: int = 64, q: int = 5):
+        import torch
+        self.instance, self.batch = instance, batch
+        self.rng = R.philox_generator(A.worker_seed(seed, 7100), R.ALNS_STREAM)
+        self.cur, self.zcur = start, evaluate(instance, start).makespan
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.q = min(q if instance.n < 500 else 2, instance.n)  # removals cascade; large n: smaller kicks
+        self.last_s = 0.0  # duration of the last kick step (repairs do not watch the clock)
+
+    def adopt(self, z: float, sol: Solution) -> None:
+        if z < self.zcur:
+            self.cur, self.zcur = sol, z
+
+    def round(self, deadline: float):
+        import numpy as np
+        import torch
+        from . import baselines as BL
+        from . import device as DV
+        from . import insertion as INS
+        instance, batch, dev, n = self.instance, self.batch, self.dev, self.instance.n
         tk = time.perf_counter()
-        o, l = cur.to_arrays(n)
+        o, l = self.cur.to_arrays(n)
         ops = torch.from_numpy(np.tile(o[:2 * n], (batch, 1))).to(dev)
         lens = torch.from_numpy(np.tile(l, (batch, 1))).to(dev)
         gens = [np.random.Generator(np.random.Philox(key=(int(x), 0xC1C)))
-                for x in rng.integers(0, 2**62, size=batch)]
+                for x in self.rng.integers(0, 2**62, size=batch)]
         states = torch.from_numpy(np.stack([R.state_bytes(g) for g in gens])).to(dev)
         d = DV.destroy_batch(instance, ops, lens, torch.zeros(batch, dtype=torch.int32, device=dev),
-                             torch.full((batch,), qq, dtype=torch.int32, device=dev),
+                             torch.full((batch,), self.q, dtype=torch.int32, device=dev),
                              min(A.removal_bounds(n)[0], n), states)
         nr = d["nremoved"].cpu().numpy()
         rem = d["removed"].cpu().numpy()
         ro, rl, st = INS.reinsert_batch(instance, d["ops"], d["lens"], [list(rem[i, :nr[i]]) for i in range(batch)],
                                         [0] * batch, None)
         ok = np.flatnonzero(st == 0)
+        self.last_s = time.perf_counter() - tk
         if not ok.size:
-            continue
+            return None
         z = DV.makespan_batch(instance, ro[ok], rl[ok], mode=0)
         zs, ss = z["z"].cpu().numpy(), z["status"].cpu().numpy()
         good = np.flatnonzero(ss == 0)
         if not good.size:
-            continue
+            return None
         k = ok[good[np.argmin(zs[good])]]
         kicked = Solution.from_arrays(ro[k], rl[k])
-        kick_s = time.perf_counter() - tk
+        self.last_s = time.perf_counter() - tk
         pol = BL.two_opt_improve(instance, kicked, move_budget=10**15, resume=True, deadline=deadline)
         zp = evaluate(instance, pol).makespan
-        if zp < zcur:
-            cur, zcur = pol, zp
-            yield pol
+        if zp < self.zcur:
+            self.cur, self.zcur = pol, zp
+            return pol
+        return None
 
 
 def run_pipeline_budget_distributed(instance, seconds: float, seed: int = 0, group=None, **kw):
     """run_pipeline_budget on every rank of ``group`` (one GPU each; SURVEY
     §8(e): the pipeline's work shards as independent searches) with
-    rank-specific seeds, followed by a min-all-reduce of the best makespan
-    and a broadcast of the winner's routes (alns.sync_pool_share: lowest
-    rank wins ties).  Every rank returns (best Solution, best makespan,
+    rank-specific seeds.  The ranks cooperate: at every stage boundary and
+    after every kick round of the tail they min-all-reduce the best makespan
+    and broadcast the winner's routes (alns.sync_pool_share: lowest rank wins
+    ties), and continue from the global best; a final exchange makes the
+    result identical on every rank.  Every rank returns (best Solution, best makespan,
     its own trace)."""
-    rank, _ = A._dist_world(group)
-    sol, z, trace = run_pipeline_budget(instance, seconds, seed=seed + 1009 * rank, **kw)
+    rank, world = A._dist_world(group)
+
+    def exchange(z, sol, more):
+        if world < 2:
+            return z, sol, more
+        import torch
+        import torch.distributed as dist
+        share = A._PoolShare()
+        share.offer(rank, z, sol)
+        A.sync_pool_share(instance, share, group)
+        dev = (torch.device("cuda", torch.cuda.current_device())
+               if dist.get_backend(group) == "nccl" else torch.device("cpu"))
+        flag = torch.tensor([1 if more else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        return share.best_z, share.best_sol, bool(flag.item())
+
+    sol, z, trace = run_pipeline_budget(instance, seconds, seed=seed + 1009 * rank, exchange=exchange, **kw)
     share = A._PoolShare()
     share.offer(rank, z, sol)
     A.sync_pool_share(instance, share, group)

@@ -22,6 +22,9 @@ def timed(*a, **k):
 
 BL.two_opt_improve = timed
 last = time.perf_counter()
-for s in P._kick_and_polish(inst, sol, t + secs, 0):
-    print(f"improved {evaluate(inst, s).makespan:.0f} at {time.perf_counter() - t:.1f}s", flush=True)
+kick = P._Kicker(inst, sol, 0)
+while time.perf_counter() + 1.2 * kick.last_s < t + secs - 0.5:
+    s = kick.round(t + secs)
+    if s is not None:
+        print(f"improved {evaluate(inst, s).makespan:.0f} at {time.perf_counter() - t:.1f}s", flush=True)
 print(f"ILS ended at {time.perf_counter() - t:.1f}s (deadline {secs}s)", flush=True)

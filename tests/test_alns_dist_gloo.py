@@ -90,14 +90,26 @@ def _pipeline_case(rank, world):
     from conftest import config_instance
     from paper_2602_23685_b200.pipeline import run_pipeline_budget_distributed
     from paper_2602_23685_b200.schedule import evaluate
+    from paper_2602_23685_b200 import alns as A
+    calls = []
+    orig = A.sync_pool_share
+
+    def counted(*a, **k):
+        calls.append(1)
+        return orig(*a, **k)
+    A.sync_pool_share = counted
     inst = config_instance("gr17")
     sol, z, trace = run_pipeline_budget_distributed(inst, seconds=3.0, pool_size=8)
-    return z, evaluate(inst, sol).makespan, min(b for _, b in trace), sol.to_arrays(inst.n)[0].tolist()
+    return (z, evaluate(inst, sol).makespan, min(b for _, b in trace), sol.to_arrays(inst.n)[0].tolist(),
+            len(calls))
 
 
 @pytest.mark.gpu
 def test_pipeline_budget_distributed_world2_on_one_gpu():
     out = run_world(_pipeline_case)
-    (z0, e0, own0, s0), (z1, e1, own1, s1) = out[0], out[1]
+    (z0, e0, own0, s0, c0), (z1, e1, own1, s1, c1) = out[0], out[1]
     assert z0 == z1 == e0 == e1 and s0 == s1  # one global best everywhere
     assert z0 == min(own0, own1)
+    # the ranks cooperate during the budget: the same number of incumbent
+    # exchanges on both (stage boundaries + every kick round + the final one)
+    assert c0 == c1 >= 4
