@@ -453,11 +453,17 @@ struct MultiLayout {
     size_t pend, ready, hint, total;
 };
 
+// ready_bytes = 0: the compact slot table (CT) -- a u8 slot id per customer
+// plus MULTI_SLOTS uint32 ready values (see decode_multi_kernel)
+constexpr int MULTI_SLOTS = 32;
+
 __host__ __device__ inline MultiLayout multi_layout(int n, int ready_bytes) {
     MultiLayout L;
     L.pend = 0;
     L.ready = align16(2 * (size_t)(2 * n));
-    L.hint = L.ready + align16((size_t)ready_bytes * (size_t)(n + 1));
+    const size_t rb = ready_bytes ? align16((size_t)ready_bytes * (size_t)(n + 1))
+                                  : align16((size_t)(n + 1)) + 4 * MULTI_SLOTS;
+    L.hint = L.ready + rb;
     L.total = L.hint + align16((size_t)(2 * n));
     return L;
 }
@@ -483,7 +489,14 @@ __device__ __forceinline__ void seg_flags(bool vlane, double t, int net, int lo,
     pick_maxT = relax ? 0.0 : seg_max<P>(cp ? t : -DBL_MAX);
 }
 
-template <bool INTD, typename OutT, bool NARROW, int P, int MC = 0>  // MC: as decode_kernel
+// CT (with NARROW): the ready table is a slot table, as in K1 -- customers
+// dropped but not yet picked up number at most sum_v q0_v <= m k (the decoder
+// keeps every vehicle's load interval feasible), so m k <= 32 slots of uint32
+// values and a u8 slot id per customer replace the (n+1)-entry table: 5 KB
+// less shared memory per chromosome at n = 999, twice the resident
+// chromosomes.  A chromosome that finds no free slot goes to the wide fix-up
+// pass like a 32-bit overflow.
+template <bool INTD, typename OutT, bool NARROW, int P, int MC = 0, bool CT = false>  // MC: as decode_kernel
 __global__ void __launch_bounds__(256, 4)
 decode_multi_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, int64_t N,
                     int relax, double penalty, double *__restrict__ fitness_out,
@@ -499,9 +512,11 @@ decode_multi_kernel(DevInstance I, const double *__restrict__ genes, int64_t gst
     const int seg = lane / P, sl = lane % P, sbase = seg * P;
     const unsigned smask = (P == 32) ? 0xffffffffu : (((1u << P) - 1u) << sbase);
     const int n = I.n, m = MC ? MC : I.m, k = I.k, two_n = 2 * n;
-    const MultiLayout Ly = multi_layout(n, (int)sizeof(RT));
+    const MultiLayout Ly = multi_layout(n, CT ? 0 : (int)sizeof(RT));
     unsigned char *base = smem + ((size_t)warp * G + seg) * Ly.total;
     volatile RT *s_ready = reinterpret_cast<volatile RT *>(base + Ly.ready);
+    volatile uint8_t *s_sid = reinterpret_cast<volatile uint8_t *>(base + Ly.ready);
+    volatile uint32_t *s_val = reinterpret_cast<volatile uint32_t *>(base + Ly.ready + align16((size_t)(n + 1)));
     uint16_t *s_pend = reinterpret_cast<uint16_t *>(base + Ly.pend);
     int8_t *s_hint = reinterpret_cast<int8_t *>(base + Ly.hint);
     const bool vlane = sl < m;
@@ -522,9 +537,15 @@ decode_multi_kernel(DevInstance I, const double *__restrict__ genes, int64_t gst
                 s_pend[i] = __ldg(ord + i);
                 s_hint[i] = (int8_t)hint_vehicle(m, __ldg(g + two_n + i));
             }
-            for (int c = sl; c <= n; c += P) s_ready[c] = NARROW ? (RT)NOT_DROPPED32 : (RT)-1.0;
+            if (CT) {
+                volatile uint32_t *w4 = reinterpret_cast<volatile uint32_t *>(s_sid);
+                for (int c = sl; c < (n + 4) / 4; c += P) w4[c] = 0xFFFFFFFFu;
+            } else {
+                for (int c = sl; c <= n; c += P) s_ready[c] = NARROW ? (RT)NOT_DROPPED32 : (RT)-1.0;
+            }
         }
         __syncwarp();
+        unsigned freem = 0xFFFFFFFFu;  // CT: free slots (segment-uniform)
 
         double t = 0.0;
         int loc = 0, net = 0, lo = 0, hi = k, cnt = 0;
@@ -571,7 +592,12 @@ decode_multi_kernel(DevInstance I, const double *__restrict__ genes, int64_t gst
                     pk = op & 1;
                     hj = valid ? s_hint[op] : 0;
                     pj = valid && !pk ? __ldg(I.p + c) : 0.0;
-                    rr = pk ? s_ready[c] : (RT)0;
+                    if (CT) {
+                        const int sd = pk ? (int)s_sid[c] : 0xFF;
+                        rr = pk ? (sd == 0xFF ? (RT)NOT_DROPPED32 : (RT)s_val[sd & (MULTI_SLOTS - 1)]) : (RT)0;
+                    } else {
+                        rr = pk ? s_ready[c] : (RT)0;
+                    }
                 }
                 const unsigned vb = __ballot_sync(VRP_FULL_MASK, valid);
                 if (refill) todo = vb & smask;
@@ -658,8 +684,18 @@ decode_multi_kernel(DevInstance I, const double *__restrict__ genes, int64_t gst
                     } else {
                         rs = (RT)rv;
                     }
-                    if (sl == 0) s_ready[cf] = rs;
+                    if (CT) {
+                        ovf |= freem == 0u;  // no free slot: the wide fix-up pass decodes it
+                        const int slot = freem ? __ffs(freem) - 1 : 0;
+                        freem &= ~(1u << slot);
+                        if (sl == 0) { s_val[slot] = (uint32_t)rs; s_sid[cf] = (uint8_t)slot; }
+                    } else {
+                        if (sl == 0) s_ready[cf] = rs;
+                    }
                     if (op == opf + 1) rr = rs;  // the window holds the pickup
+                } else if (CT) {
+                    const int sd = (int)s_sid[cf];  // its dropoff's slot is free again
+                    freem |= 1u << (sd & (MULTI_SLOTS - 1));
                 }
                 if (sl == 0 && seq) seq[nseq] = (uint32_t)opf | ((uint32_t)vstar << 16);
                 ++nseq;
@@ -740,14 +776,14 @@ int plan_decode(Kern kern, size_t per_warp, DecodePlan &out) {
     return 0;
 }
 
-template <bool INTD, typename OutT, bool NARROW, int P, int MC = 0>
+template <bool INTD, typename OutT, bool NARROW, int P, int MC = 0, bool CT = false>
 int launch_m(const DevInstance &I, const double *genes, int64_t gstride, int64_t N, int relax,
              double penalty, double *fitness, double *makespan, int32_t *scheduled, int64_t *visits,
              void *ops_out, int64_t ostride, int32_t *lens_out, const uint16_t *order, uint32_t *seq,
              uint8_t *retry, const uint8_t *only, cudaStream_t stream, int sm_count) {
     constexpr int G = 32 / P;
-    auto kern = decode_multi_kernel<INTD, OutT, NARROW, P, MC>;
-    const size_t per_warp = multi_layout(I.n, NARROW ? 4 : 8).total * G;
+    auto kern = decode_multi_kernel<INTD, OutT, NARROW, P, MC, CT>;
+    const size_t per_warp = multi_layout(I.n, CT ? 0 : (NARROW ? 4 : 8)).total * G;
     static PlanCache<DecodePlan> cache;
     DecodePlan pl;
     const int rc = cache.get((int64_t)per_warp, pl, [&](DecodePlan &out) { return plan_decode(kern, per_warp, out); });
@@ -799,10 +835,20 @@ int launch_any(const DevInstance &I, const double *genes, int64_t gstride, int64
                void *ops_out, int64_t ostride, int32_t *lens_out, const uint16_t *order, uint32_t *seq,
                uint8_t *retry, const uint8_t *only, cudaStream_t stream, int sm_count) {
     const char *single = getenv("VRP_DECODE_SINGLE");
-    // below n = 500 (a280: 2.8 KB of shared memory per chromosome); at n = 999
-    // (10 KB) residency drops to ~20 chromosomes per SM and the warp-per-
-    // chromosome kernel is 2.8x faster (measured)
+    const char *noct = getenv("VRP_DECODE_NO_CT");  // (ablation knob)
+    // the compact slot table (narrow pass, m k <= 32 slots, m = 6): 5 KB of
+    // shared memory per chromosome at n = 999 instead of 10 KB
+    const bool ct = NARROW && I.m == 6 && I.m * I.k <= MULTI_SLOTS && !(noct && noct[0] && noct[0] != '0');
+    // below n = 500 (a280: 2.8 KB of shared memory per chromosome; the slot
+    // table measured +15 % generations/s there).  At n = 999 the warp-per-
+    // chromosome kernel wins: 2.8x with the full table, and still 2x with the
+    // slot table (random chromosomes defer ~11 ops per placement there, and
+    // its 32-op pending window scans 4x faster than a segment's 8-op window)
     const bool seg = !(single && single[0] && single[0] != '0') && I.n < 500;
+    if (seg && ct)
+        return launch_m<INTD, OutT, NARROW, 8, 6, true>(I, genes, gstride, N, relax, penalty, fitness, makespan,
+                                                        scheduled, visits, ops_out, ostride, lens_out, order, seq,
+                                                        retry, only, stream, sm_count);
     if (seg && I.m == 6)  // the fleet of every benchmark config beyond gr17
         return launch_m<INTD, OutT, NARROW, 8, 6>(I, genes, gstride, N, relax, penalty, fitness, makespan,
                                                   scheduled, visits, ops_out, ostride, lens_out, order, seq, retry,
