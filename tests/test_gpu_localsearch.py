@@ -7,6 +7,7 @@ import torch
 import inputs as I
 from conftest import config_instance
 from oracle import oracle as O
+import ls_host_ref as H
 from paper_2602_23685_b200 import alns as A
 from paper_2602_23685_b200 import localsearch as LS
 from paper_2602_23685_b200.schedule import Solution, exact_makespan
@@ -36,8 +37,8 @@ def test_batched_local_search_vs_host_neighbourhoods(key, count):
     genes = I.chromosomes(inst.n, count, (83, CID[key]))
     dec = O.decode_batch(inst, genes)
     ops, lens = dec["ops"], dec["lens"]
-    for kind, fn, host in ((0, LS.pickup_repositioning_batch, A._pickup_repositioning_host),
-                           (1, LS.cross_agent_relocation_batch, A._cross_agent_relocation_host)):
+    for kind, fn, host in ((0, LS.pickup_repositioning_batch, H.pickup_repositioning_host),
+                           (1, LS.cross_agent_relocation_batch, H.cross_agent_relocation_host)):
         o, l, z = fn(inst, ops, lens)
         o, l = o.cpu().numpy(), l.cpu().numpy()
         for j in range(count):
