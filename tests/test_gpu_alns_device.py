@@ -211,3 +211,25 @@ def test_reference_signature_destroy_and_removal_api(golden, golden_meta):
             gains = INS.removal_gains(inst, Solution.from_arrays(o, l))
             want = DO.removal_gains(inst, o, l)
             assert [gains[c] for c in inst.customers] == list(want[1:]), key
+
+
+def test_removal_api_on_partial_solutions(golden):
+    """insertion.removal_gains / remove_customers (K6 device code) on partial
+    solutions -- customers absent from every route -- against the oracle."""
+    from paper_2602_23685_b200 import insertion as INS
+    for key in ("eil51", "a280", "dsj1000"):
+        inst = config_instance(key)
+        o, l = golden[f"{key}/dec_ops"][1], golden[f"{key}/dec_lens"][1]
+        pick = I.philox(91, CID[key]).choice(np.arange(1, inst.n + 1), size=5, replace=False)
+        po, pl, rem = O.remove_customers(inst, o, l, pick)
+        part = Solution.from_arrays(po, pl)
+        gains = INS.removal_gains(inst, part)
+        want = DO.removal_gains(inst, po, pl)
+        assert [gains[c] for c in inst.customers] == list(want[1:]), key
+        more = I.philox(92, CID[key]).choice(np.setdiff1d(np.arange(1, inst.n + 1), rem), size=3, replace=False)
+        tours, removed = INS.remove_customers(inst, part, [int(c) for c in more])
+        wo, wl, wr = O.remove_customers(inst, po, pl, more)
+        assert removed == [int(c) for c in wr], key
+        to, tl = Solution.from_lists(tours).to_arrays(inst.n)
+        np.testing.assert_array_equal(tl, wl)
+        np.testing.assert_array_equal(to[:int(tl.sum())], wo[:int(wl.sum())])

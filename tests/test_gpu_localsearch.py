@@ -75,3 +75,44 @@ def test_builder_covers_whole_neighbourhood():
         assert sorted(b_ops[j].tolist()) == sorted(o.tolist())
         seen.add(tuple(b_ops[j].tolist()) + tuple(b_lens[j].tolist()))
     assert len(seen) == total
+
+
+def test_ls_topk_kernel_vs_numpy():
+    """vrp_ls_topk: per solution, the K smallest (estimate, generation index)
+    survivors (status 0, estimate < threshold) over several chunks -- the
+    reference's stable sort + [:_VERIFY_LIMIT] -- against numpy."""
+    from paper_2602_23685_b200 import _native as N
+    from paper_2602_23685_b200.localsearch import _segments
+    g = np.random.default_rng(5)
+    W, K = 7, 10
+    sizes = np.array([0, 5, 3000, 1, 9000, 17, 4200])  # candidates per solution (ranges ascending)
+    wb = np.concatenate([[0], np.cumsum(sizes)[:-1]])
+    we = wb + sizes
+    total = int(sizes.sum())
+    z = np.round(g.random(total) * 50) / 4  # many ties
+    st = (g.random(total) < 0.1).astype(np.int32)
+    thr = g.random(W) * 12
+    wid = np.flatnonzero(sizes > 0)
+    dev = torch.device("cuda")
+    top_z = torch.empty((W, K), dtype=torch.float64, device=dev)
+    top_i = torch.empty((W, K), dtype=torch.int64, device=dev)
+    top_n = torch.from_numpy(np.zeros(W, np.int32)).to(dev)
+    zthr = torch.from_numpy(thr).to(dev)
+    chunk = 2500
+    for first in range(0, total, chunk):
+        cnt = min(chunk, total - first)
+        zz = torch.from_numpy(z[first:first + cnt].copy()).to(dev)
+        ss = torch.from_numpy(st[first:first + cnt].copy()).to(dev)
+        tabs = [torch.from_numpy(x).to(dev) for x in _segments(wid, wb[wid], we[wid], first, cnt)]
+        seg_w, seg_b, seg_e, ws, wf, wc = tabs
+        N.check(N.lib().vrp_ls_topk(N.ptr(zz), N.ptr(ss), first, N.ptr(zthr), N.ptr(seg_w), N.ptr(seg_b),
+                                    N.ptr(seg_e), seg_w.numel(), N.ptr(ws), N.ptr(wf), N.ptr(wc), ws.numel(), K,
+                                    N.ptr(top_z), N.ptr(top_i), N.ptr(top_n), N.stream_handle()), "vrp_ls_topk")
+    tn, tz, ti = top_n.cpu().numpy(), top_z.cpu().numpy(), top_i.cpu().numpy()
+    for w in range(W):
+        idx = np.arange(wb[w], we[w])
+        ok = idx[(st[idx] == 0) & (z[idx] < thr[w])]
+        order = ok[np.lexsort((ok, z[ok]))][:K]  # stable by estimate
+        assert tn[w] == order.size, w
+        np.testing.assert_array_equal(ti[w, :tn[w]], order)
+        np.testing.assert_array_equal(tz[w, :tn[w]], z[order])
