@@ -70,7 +70,8 @@ __host__ __device__ inline CandLayout cand_layout(int n, int mode, int ready_byt
         L.vals = L.freem = 0;
     }
     L.bits = o;  if (mode != MODE_EXACT) o += align16(sizeof(uint32_t) * (size_t)((2 * n + 31) / 32));
-    L.posd = o;  if (mode == MODE_TWO) o += align16(sizeof(uint32_t) * (size_t)(n + 1));
+    // two-pass: the dropoff route of every customer, u8 (bit 7: passed by pass 2)
+    L.posd = o;  if (mode == MODE_TWO) o += align16((size_t)(n + 1));
     L.total = o;
     return L;
 }
@@ -209,7 +210,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     RT *s_ready = reinterpret_cast<RT *>(cbase + CL.ready);
     uint8_t *s_sid = cbase + CL.ready;
     uint32_t *s_val = reinterpret_cast<uint32_t *>(cbase + CL.vals);
-    uint32_t *s_posd = reinterpret_cast<uint32_t *>(cbase + CL.posd);
+    uint8_t *s_posd = cbase + CL.posd;
 
     for (int c = threadIdx.x; c <= n; c += blockDim.x)
         s_p[c] = INTD ? (TT)__ldg(I.p32 + c) : (TT)__ldg(I.p + c);
@@ -291,7 +292,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                     const TT rv = t + s_p[c];
                     if (NARROW) ovf |= rv < t;
                     s_ready[c] = (RT)rv;
-                    s_posd[c] = ((uint32_t)v << 16) | (uint32_t)rs.i;
+                    s_posd[c] = (uint8_t)v;  // every customer's dropoff route (valid candidates: each once)
                 }
                 cap_step(op, k, s, lo, hi);
                 lastc = c;
@@ -312,8 +313,11 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 if (op & 1) {
                     const TT r = (TT)s_ready[c];
                     if (r > t) t = r;
-                    const uint32_t pd = s_posd[c];
-                    dead |= (int)(pd >> 16) == v && (int)(pd & 0xffffu) > rs.i;
+                    // its dropoff is on this route and not passed yet: a pickup before it
+                    const int pd = s_posd[c];
+                    dead |= (pd & 0x7F) == v && !(pd & 0x80);
+                } else {
+                    s_posd[c] = (uint8_t)(v | 0x80);  // only this lane touches route v's dropoffs
                 }
                 rs.advance(I);
             }
