@@ -248,6 +248,52 @@ __global__ void __launch_bounds__(256) stream_rows_kernel(const vrp_philox *__re
     }
 }
 
+// Offspring row r (mask words mask0 + r*G ..): phase 1, one thread per Philox
+// block, writes the row's mask verdicts (u < bias) to shared memory; phase 2
+// copies both parents 16 bytes at a time and selects per gene (both parents'
+// sectors are fetched either way -- the mask is random per gene).
+__global__ void __launch_bounds__(256) offspring_rows_kernel(const vrp_philox *__restrict__ Sp, EvolveShape sh,
+                                                             const double *__restrict__ pop,
+                                                             const int32_t *__restrict__ order,
+                                                             const int32_t *__restrict__ e_idx,
+                                                             const int32_t *__restrict__ o_idx,
+                                                             const unsigned long long *__restrict__ u32_used,
+                                                             double bias, double *__restrict__ out, int64_t row0) {
+    extern __shared__ uint8_t s_mask[];
+    const vrp_philox S = *Sp;
+    const int64_t G = sh.G, r = row0 + blockIdx.y;
+    const int64_t head = 4 - (int64_t)S.buffer_pos;
+    const int64_t q0 = (int64_t)(sh.n_mutant * G) + (int64_t)u64s_for_u32(S, *u32_used) + r * G;
+    const int64_t qq0 = q0 - head;
+    const int64_t b0 = qq0 >= 0 ? qq0 / 4 : -((3 - qq0) / 4);
+    const int64_t nblk = (qq0 + G - 1 - 4 * b0) / 4 + 1;
+    for (int64_t j = threadIdx.x; j < nblk; j += blockDim.x) {
+        const int64_t qqb = 4 * (b0 + j);
+        uint64_t w[4];
+        if (qqb >= 0) {
+            uint64_t c[4];
+            ctr_add(S.ctr, 1 + (uint64_t)(qqb / 4), c);
+            philox_block(c[0], c[1], c[2], c[3], S.key[0], S.key[1], w);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t g = qqb + k - qq0;
+            if (g < 0 || g >= G) continue;
+            const int64_t qq = qqb + k;
+            const uint64_t x = qq >= 0 ? w[k] : S.buffer[S.buffer_pos + (qq + head)];
+            s_mask[g] = u64_to_double(x) < bias;
+        }
+    }
+    __syncthreads();
+    const double2 *pe = reinterpret_cast<const double2 *>(pop + (int64_t)order[e_idx[r]] * G);
+    const double2 *po = reinterpret_cast<const double2 *>(pop + (int64_t)order[sh.n_elite + o_idx[r]] * G);
+    double2 *dst = reinterpret_cast<double2 *>(out + (sh.n_elite + sh.n_mutant + r) * G);
+    for (int64_t j = threadIdx.x; j < G / 2; j += blockDim.x) {
+        const double2 a = __ldg(pe + j), b = __ldg(po + j);
+        dst[j] = make_double2(s_mask[2 * j] ? a.x : b.x, s_mask[2 * j + 1] ? a.y : b.y);
+    }
+}
+
 // advance the caller's generator past everything evolve consumed
 __global__ void state_kernel(vrp_philox *__restrict__ Sp, EvolveShape sh,
                              const unsigned long long *__restrict__ u32_used) {
@@ -437,9 +483,15 @@ int launch_evolve(const double *pop, const double *fit, int64_t N, int64_t G, do
         for (int64_t r0 = 0; r0 < sh.n_mutant; r0 += YMAX)
             stream_rows_kernel<false><<<dim3(bx, (unsigned)(sh.n_mutant - r0 < YMAX ? sh.n_mutant - r0 : YMAX)), 256,
                                         0, stream>>>(state, sh, pop, order, e_idx, o_idx, scal + 1, bias, out, r0);
-        for (int64_t r0 = 0; r0 < sh.n_off; r0 += YMAX)
-            stream_rows_kernel<true><<<dim3(bx, (unsigned)(sh.n_off - r0 < YMAX ? sh.n_off - r0 : YMAX)), 256, 0,
-                                       stream>>>(state, sh, pop, order, e_idx, o_idx, scal + 1, bias, out, r0);
+        for (int64_t r0 = 0; r0 < sh.n_off; r0 += YMAX) {
+            const unsigned rows = (unsigned)(sh.n_off - r0 < YMAX ? sh.n_off - r0 : YMAX);
+            if (vec && (size_t)G <= 48 * 1024)  // mask row in shared memory, 16-byte parent copies
+                offspring_rows_kernel<<<dim3(1, rows), 256, (size_t)G, stream>>>(state, sh, pop, order, e_idx, o_idx,
+                                                                             scal + 1, bias, out, r0);
+            else
+                stream_rows_kernel<true><<<dim3(bx, rows), 256, 0, stream>>>(state, sh, pop, order, e_idx, o_idx,
+                                                                            scal + 1, bias, out, r0);
+        }
     }
     state_kernel<<<1, 1, 0, stream>>>(state, sh, scal + 1);
     cudaFreeAsync(e_idx, stream);

@@ -262,3 +262,28 @@ def test_bottleneck_out_vs_oracle(key, golden):
             assert np.array_equal(r["status"].cpu().numpy(), st)
             want = np.argmax(ret, axis=1)  # first maximum (strict >), like Schedule.bottleneck
             np.testing.assert_array_equal(r["bottleneck"].cpu().numpy()[ok], want[ok], err_msg=name)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 5, 6, 7])
+def test_decode_hint_vehicle_edge_values_on_device(m, golden):
+    """_hint_vehicle (brkga.py:82-89) on the device at the reference's edge
+    values (golden hint/genes: m*g - h within 1e-9 of 1, exact multiples,
+    1 - ulp): with capacity for everything every hint vehicle is feasible, so
+    the decoded vehicle of each op IS the device's hint; decode must equal the
+    oracle's (whose hint is pinned to the reference's goldens)."""
+    from paper_2602_23685_b200.instance import Instance
+    base = config_instance("gr17")
+    d, p = base.arrays()
+    inst = Instance.from_arrays(d, p, m, base.n, label=f"gr17-m{m}")
+    edge = np.asarray(golden["hint/genes"], dtype=np.float64)
+    edge = edge[(edge >= 0.0) & (edge < 1.0)]
+    n = inst.n
+    rows = 64
+    genes = I.chromosomes(n, rows, (93, m))
+    hints = np.resize(edge, rows * 2 * n).reshape(rows, 2 * n)
+    genes[:, 2 * n:] = hints
+    r = dev().decode_batch(inst, _cuda(genes))
+    ref = O.decode_batch(inst, genes)
+    np.testing.assert_array_equal(r["lens"].cpu().numpy(), ref["lens"])
+    np.testing.assert_array_equal(r["ops"].cpu().numpy(), ref["ops"])
+    np.testing.assert_array_equal(r["fitness"].cpu().numpy(), ref["fitness"])
