@@ -200,25 +200,28 @@ def decode_batch(instance, genes, relax: bool = True, penalty: float = 1e6,
     return res
 
 
+N_STREAMS = 2  # copy/compute streams of score_host_batch
+
+
 def _pipeline(di, chunk: int, op_dtype):
     # held by the DeviceInstance (one device each), so the buffers live exactly
     # as long as the instance
     pipes = di.__dict__.setdefault("_pipes", {})
-    key = (chunk, op_dtype)
+    key = (chunk, op_dtype, N_STREAMS)
     st = pipes.get(key)
     if st is None:
         dev = torch.device("cuda", torch.cuda.current_device())
-        st = {"streams": [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)],
+        st = {"streams": [torch.cuda.Stream(device=dev) for _ in range(N_STREAMS)],
               "bufs": [{"ops": torch.empty((chunk, 2 * di.n), dtype=op_dtype, device=dev),
                         "lens": torch.empty((chunk, di.m), dtype=torch.int32, device=dev),
                         "z": torch.empty(chunk, dtype=torch.float64, device=dev),
                         "status": torch.empty(chunk, dtype=torch.int32, device=dev)}
-                       for _ in range(2)]}
+                       for _ in range(N_STREAMS)]}
         pipes[key] = st
     return st
 
 
-def score_host_batch(instance, ops, lens, mode: int = N.MODE_EXACT, chunk: int = 1 << 16):
+def score_host_batch(instance, ops, lens, mode: int = N.MODE_EXACT, chunk: int = 1 << 14):
     """End-to-end scoring of HOST candidates: chunks are copied host->device,
     scored by K1/K2 and their (z, status) copied back, alternating two CUDA
     streams so the PCIe transfers overlap the kernel.  ``ops``/``lens`` should
@@ -241,7 +244,7 @@ def score_host_batch(instance, ops, lens, mode: int = N.MODE_EXACT, chunk: int =
     for i, a in enumerate(range(0, Nc, chunk)):
         b = min(Nc, a + chunk)
         c = b - a
-        s, buf = st["streams"][i & 1], st["bufs"][i & 1]
+        s, buf = st["streams"][i % len(st["streams"])], st["bufs"][i % len(st["bufs"])]
         with torch.cuda.stream(s):
             buf["ops"][:c].copy_(ops[a:b], non_blocking=True)
             buf["lens"][:c].copy_(lens[a:b], non_blocking=True)

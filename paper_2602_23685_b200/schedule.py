@@ -283,7 +283,7 @@ def pack_solutions(instance, solutions, op_dtype=np.int32):
     return ops, lens
 
 
-def score_host_batch(instance, ops, lens, mode: int = N.MODE_EXACT, chunk: int = 1 << 16):
+def score_host_batch(instance, ops, lens, mode: int = N.MODE_EXACT, chunk: int = 1 << 14):
     """Host candidates in, host (z, status) out; pipelined H2D / K1 / D2H."""
     from .device import score_host_batch as _s
     return _s(instance, ops, lens, mode=mode, chunk=chunk)
