@@ -214,7 +214,10 @@ def extra_rates(device, ops, lens, decode_ms, n_dec, pipeline_seconds=30.0):
     # K1 on the other benchmark configs (decoded candidates, device-resident)
     for key in ("eil51", "kroA100", "a280"):
         ki = config_instance(key)
-        cnt = 1 << 19
+        # 2^20 candidates: larger than L2 at every n (at eil51, 2^19 freshly
+        # decoded candidates sit in L2 and measure ~40 % slower than streamed
+        # from HBM -- scripts/probe_k1_addr.py)
+        cnt = 1 << 20
         kops = torch.empty((cnt, 2 * ki.n), dtype=torch.int16, device=device)
         klens = torch.empty((cnt, ki.m), dtype=torch.int32, device=device)
         kg = torch.Generator(device=device).manual_seed(11)

@@ -190,9 +190,10 @@ struct UnitRes {
     Key dk[3];     // re-timed shortlist keys (cost, d_stale, g_drop) in shortlist order
     Key pbest[3];  // per shortlist entry: argmin pickup key (cost, stale, vp, gp)
     int ns, dbest, dwin, dmask;
-    int np[3], pwin[3];
+    int np[3], pwin[3], prank[3];
     int4 sum;      // what the draw pass reads, packed for one 16-byte load:
-                   // x = ns | dbest << 4 | dwin << 8 | dmask << 12 | (np[j] > 0) << (16 + j); y, z, w = pwin[0..2]
+                   // x = ns | dbest << 4 | dwin << 8 | dmask << 12 | (np[j] > 0) << (16 + j);
+                   // y, z, w = pwin[j] | prank[j] << 16 (both < 2^16: P gaps <= 2n + m + 2)
 };
 
 // Phase C1 decisions per (customer, vd).
@@ -419,7 +420,7 @@ __device__ void priv_fast(const Ctx &X, TeamWS &W, const TeamCx &cx, int vd, int
 //   select >= 0: the select-th window member (limit given)
 struct PScan {
     Key best;
-    int np, win;
+    int np, win, brank;  // brank: window members before the argmin (flat order)
 };
 
 __device__ PScan pscan(const Ctx &X, TeamWS &W, const GapRec *crecs, int vd, int g_drop, int c, int d_stale,
@@ -433,7 +434,7 @@ __device__ PScan pscan(const Ctx &X, TeamWS &W, const GapRec *crecs, int vd, int
     bool have = false;
     int cnt = 0, seen = 0, F0 = 0;
     PScan out{};
-    out.np = 0; out.win = 0; out.best = Key{0, 0, -1, -1, 0};
+    out.np = 0; out.win = 0; out.brank = 0; out.best = Key{0, 0, -1, -1, 0};
     for (int v = 0; v < m; ++v) {
         const bool priv = v == vd;
         const int L = priv ? W.L : X.Lr[v];
@@ -507,9 +508,15 @@ __device__ PScan pscan(const Ctx &X, TeamWS &W, const GapRec *crecs, int vd, int
     if (want_win && out.np) {
         __syncwarp();
         const double lim = bk.cost * (1.0 + 0.02) + 1e-12;
-        int w = 0;
-        for (int F = lane; F < F0; F += 32) w += W.pcost[F] <= lim;
+        const int Fb = W.pstart[bk.a] + (bk.b - (bk.a == vd ? g_drop + 1 : 0));  // the argmin's flat index
+        int w = 0, wb = 0;
+        for (int F = lane; F < F0; F += 32) {
+            const bool in = W.pcost[F] <= lim;
+            w += in;
+            wb += in && F < Fb;
+        }
         out.win = warp_sum(w);
+        out.brank = warp_sum(wb);
     }
     return out;
 }
@@ -589,14 +596,15 @@ __device__ void unit_ab(Ctx &X, TeamWS &W, const GapRec *crecs, const TeamCx &cx
         VRP_UT(2);
         const PScan ps = pscan(X, W, crecs, vd, dk[j].a, c, dk[j].stale, use_rng, -1, 0.0);
         VRP_UT(3);
-        if (lane == 0) { U.np[j] = ps.np; U.pwin[j] = ps.win; U.pbest[j] = ps.best; }
+        if (lane == 0) { U.np[j] = ps.np; U.pwin[j] = ps.win; U.prank[j] = ps.brank; U.pbest[j] = ps.best; }
         __syncwarp();
     }
     if (lane == 0) {
         int x = ns | best << 4 | wcount << 8 | mask << 12;
         for (int j = 0; j < ns; ++j)
             if ((mask >> j & 1) && U.np[j] > 0) x |= 1 << (16 + j);
-        U.sum = make_int4(x, (mask & 1) ? U.pwin[0] : 0, (mask & 2) ? U.pwin[1] : 0, (mask & 4) ? U.pwin[2] : 0);
+        auto pw = [&](int j) { return (mask >> j & 1) ? (U.pwin[j] | U.prank[j] << 16) : 0; };
+        U.sum = make_int4(x, pw(0), pw(1), pw(2));
     }
     __syncwarp();
 }
@@ -689,8 +697,13 @@ __device__ int reinsert_team(Ctx &X, TeamWS &W, TeamCtl &T, UnitRes *units, Unit
                             if (x >> (16 + alt) & 1) {
                                 has = 1;
                                 ++nopt;
-                                const int pw = alt == 0 ? pw0 : alt == 1 ? pw1 : pw2;
-                                if (use_rng && pw > 1) { jp = (int)gen->integers((uint32_t)pw); ++npend; }
+                                const int pp = alt == 0 ? pw0 : alt == 1 ? pw1 : pw2;
+                                const int pw = pp & 0xFFFF, brank = pp >> 16;
+                                if (use_rng && pw > 1) {
+                                    jp = (int)gen->integers((uint32_t)pw);
+                                    if (jp == brank) jp = -1;  // the draw chose the argmin: no phase-D work
+                                    else ++npend;
+                                }
                             }
                         }
                         UnitPick &P = picks[u];

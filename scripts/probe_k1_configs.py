@@ -5,9 +5,9 @@ sys.path.insert(0, ".")
 import torch  # noqa: E402
 from paper_2602_23685_b200 import configs, device as D  # noqa: E402
 
-for key in ("gr17", "eil51", "kroA100", "a280", "dsj1000"):
+for key in (sys.argv[1:] or ("gr17", "eil51", "kroA100", "a280", "dsj1000")):
     inst = configs.config_instance(key)
-    N = 1 << 20 if inst.n < 500 else 1 << 19
+    N = int(__import__("os").environ.get("NCAND", 1 << 20 if inst.n < 500 else 1 << 19))
     ops = torch.empty((N, 2 * inst.n), dtype=torch.int16, device="cuda")
     lens = torch.empty((N, inst.m), dtype=torch.int32, device="cuda")
     gen = torch.Generator("cuda").manual_seed(5)
@@ -32,4 +32,5 @@ for key in ("gr17", "eil51", "kroA100", "a280", "dsj1000"):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 5
-    print(f"{key:8s} n={inst.n:4d}: K1 {N / ms / 1e3:8.1f} M evals/s   K3 {N / dec_ms / 1e3:6.2f} M decodes/s", flush=True)
+    bad = int((out["status"] != 0).sum())
+    print(f"{key:8s} n={inst.n:4d}: K1 {N / ms / 1e3:8.1f} M evals/s   K3 {N / dec_ms / 1e3:6.2f} M decodes/s  (non-OK statuses: {bad})", flush=True)
