@@ -105,9 +105,9 @@ repair_kernel(DevInstance I, const int32_t *__restrict__ pops, int64_t pstride,
     }
 }
 
-// The same repair with a CTA of TEAM_WARPS warps per instance (repair_team.cuh):
+// The same repair with a CTA of REPAIR_TEAM_WARPS warps per instance (repair_team.cuh):
 // integral instances with long routes (use_scan).
-__global__ void __launch_bounds__(32 * TEAM_WARPS)
+__global__ void __launch_bounds__(32 * REPAIR_TEAM_WARPS)
 repair_team_kernel(DevInstance I, const int32_t *__restrict__ pops, int64_t pstride,
                    const int32_t *__restrict__ plens, const int32_t *__restrict__ removed, int64_t rstride,
                    const int32_t *__restrict__ nremoved, const int32_t *__restrict__ regret_k,
@@ -202,10 +202,10 @@ int launch_repair(const DevInstance &I, const int32_t *pops, int64_t pstride, co
                   int32_t *out_lens, int32_t *status, int64_t N, cudaStream_t stream) {
     if (N <= 0) return 0;
     if (use_team(I)) {
-        const size_t per = al8(make_layout(I.n, I.m).total) + team_bytes(I.n, I.m, TEAM_WARPS);
+        const size_t per = al8(make_layout(I.n, I.m).total) + team_bytes(I.n, I.m, REPAIR_TEAM_WARPS);
         unsigned char *scratch = nullptr;
         if (cudaMallocAsync(&scratch, per * (size_t)N, stream) != cudaSuccess) return -1;
-        repair_team_kernel<<<(unsigned)N, 32 * TEAM_WARPS, 0, stream>>>(I, pops, pstride, plens, removed, rstride,
+        repair_team_kernel<<<(unsigned)N, 32 * REPAIR_TEAM_WARPS, 0, stream>>>(I, pops, pstride, plens, removed, rstride,
                                                                       nremoved, regret_k, states, out_ops, ostride,
                                                                       out_lens, status, scratch, per, N);
         const cudaError_t e = cudaPeekAtLastError();

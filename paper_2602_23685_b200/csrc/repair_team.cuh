@@ -38,7 +38,12 @@
 
 namespace {
 
+// warps per repair CTA: the batched repair kernel (repair.cu) runs 32 (1024
+// threads; 64 registers, a few spills, measured 1.3x faster than 16 at
+// n = 999), the ALNS iteration kernel 16 (its destroy / replay code spills
+// too much at 64 registers: 16 measured 1.2x faster there)
 constexpr int TEAM_WARPS = 16;
+constexpr int REPAIR_TEAM_WARPS = 32;
 
 // The team path: integral instances with long routes (use_scan) and n >= 72
 // (2n >= 24 m at m = 6); VRP_TEAM_MIN_N (compile-time) moves the threshold.
