@@ -233,3 +233,23 @@ def test_removal_api_on_partial_solutions(golden):
         to, tl = Solution.from_lists(tours).to_arrays(inst.n)
         np.testing.assert_array_equal(tl, wl)
         np.testing.assert_array_equal(to[:int(tl.sum())], wo[:int(wl.sum())])
+
+
+@pytest.mark.parametrize("m,k,n_nodes", [(2, 6, 90), (12, 3, 160)])
+def test_team_alns_engine_other_fleet_shapes(m, k, n_nodes):
+    """vrp_alns_iterate's CTA-per-worker path on fleets other than m = 6:
+    the device engine equals the host engine (K6 + batched K5 + K1 + host
+    acceptance)."""
+    from paper_2602_23685_b200.instance import Instance
+    g = np.random.default_rng(m * 100 + k)
+    pts = g.integers(0, 500, size=(n_nodes, 2))
+    d = np.ceil(np.sqrt(((pts[:, None, :] - pts[None, :, :]) ** 2).sum(-1)))
+    p = np.concatenate([[0.0], g.integers(5, 400, size=n_nodes - 1).astype(float)])
+    inst = Instance.from_arrays(d, p, m, k, label=f"team-alns-m{m}")
+    params = A.AlnsParams(max_iter=12, weight_interval=5, stagnation_threshold=4, t0=0.05,
+                          pickup_reposition_interval=10**6, cross_agent_interval=10**6)
+    initial = A.construct_initial(inst)
+    b1, s1 = A.run_alns(inst, params, seed=9, initial=initial, engine="device")
+    b2, s2 = A.run_alns(inst, params, seed=9, initial=initial, engine="host")
+    assert b1 == b2
+    _same_stats(s1, s2)

@@ -164,3 +164,37 @@ def test_repair_batch_vs_oracle_dsj1000():
                 np.testing.assert_array_equal(o[j], ro, err_msg=str(i))
             if use:
                 assert same_state(gens[j], g), i
+
+
+@pytest.mark.parametrize("m,k,n_nodes", [(1, 40, 80), (2, 6, 90), (12, 3, 160)])
+def test_team_repair_other_fleet_shapes_vs_oracle(m, k, n_nodes):
+    """The CTA-per-repair path (integral instances with 2n >= 24 m) on fleets
+    other than the benchmark's m = 6: one vehicle, two, and twelve (more
+    routes than a 8-lane segment), against the oracle's reinsert_all."""
+    from paper_2602_23685_b200.instance import Instance
+    g = np.random.default_rng(m * 100 + k)
+    pts = g.integers(0, 500, size=(n_nodes, 2))
+    d = np.ceil(np.sqrt(((pts[:, None, :] - pts[None, :, :]) ** 2).sum(-1)))
+    p = np.concatenate([[0.0], g.integers(5, 400, size=n_nodes - 1).astype(float)])
+    inst = Instance.from_arrays(d, p, m, k, label=f"team-m{m}")
+    n = inst.n
+    assert 2 * n >= 24 * m  # the team path
+    count = 12
+    dec = O.decode_batch(inst, I.chromosomes(n, count, (95, m)))
+    parts, plens, removed, rks = [], [], [], []
+    for i in range(count):
+        pick = I.philox(96, m, i).choice(np.arange(1, n + 1), size=6, replace=False)
+        o, l, r = O.remove_customers(inst, dec["ops"][i], dec["lens"][i], pick)
+        parts.append(o[:2 * n]); plens.append(l); removed.append(r)
+        rks.append((0, 2, 3, m)[i % 4] if m > 1 else 0)
+    parts, plens = np.stack(parts), np.stack(plens)
+    gens = [I.philox(97, m, i) for i in range(count)]
+    o, l, st = INS.reinsert_batch(inst, parts, plens, removed, rks, gens)
+    for i in range(count):
+        gi = I.philox(97, m, i)
+        rst, ro, rl = O.reinsert_all(inst, parts[i], plens[i], removed[i], rks[i], gi)
+        assert st[i] == rst, i
+        if rst == 0:
+            np.testing.assert_array_equal(l[i], rl, err_msg=str(i))
+            np.testing.assert_array_equal(o[i], ro, err_msg=str(i))
+        assert same_state(gens[i], gi), i
