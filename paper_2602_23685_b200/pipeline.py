@@ -38,7 +38,7 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_
                         initial: Solution | None = None, fit_cooling: bool = True,
                         polish: bool = True, polish_share: float | None = None,
                         final_share: float | None = None,
-                        alns_max_n: int = 400, exchange=None):
+                        alns_max_n: int = 400, exchange=None, diversify: int = 0):
     """Best makespan found within a wall-clock budget (the BASELINE metric's
     'best makespan at fixed time'; the reference has no budget).
 
@@ -82,6 +82,11 @@ def run_pipeline_budget(instance, seconds: float, alns_share: float = 0.8, pool_
     z0 = evaluate(instance, init).makespan
     best = (z0, init)
     trace.append((time.perf_counter() - t0, z0))
+    if diversify:
+        # another rank of a multi-GPU run: start the (deterministic) polish from
+        # a kicked copy of the construction, so the ranks explore different
+        # local optima instead of repeating one
+        best = _Kicker(instance, init, seed + 7919 * diversify, q=10).kick()
 
     def offer(sol):
         nonlocal best
@@ -198,7 +203,13 @@ class _Kicker:
         if z < self.zcur:
             self.cur, self.zcur = sol, z
 
-    def round(self, deadline: float):
+    def kick(self):
+        """The best of one batch of kicks of the current solution (no polish):
+        (makespan, Solution); the current solution when no kick repairs."""
+        sol = self.round(None, polish=False)
+        return (evaluate(self.instance, sol).makespan, sol) if sol is not None else (self.zcur, self.cur)
+
+    def round(self, deadline, polish: bool = True):
         import numpy as np
         import torch
         from . import baselines as BL
@@ -231,6 +242,8 @@ class _Kicker:
         k = ok[good[np.argmin(zs[good])]]
         kicked = Solution.from_arrays(ro[k], rl[k])
         self.last_s = time.perf_counter() - tk
+        if not polish:
+            return kicked
         pol = BL.two_opt_improve(instance, kicked, move_budget=10**15, resume=True, deadline=deadline)
         zp = evaluate(instance, pol).makespan
         if zp < self.zcur:
@@ -242,7 +255,8 @@ class _Kicker:
 def run_pipeline_budget_distributed(instance, seconds: float, seed: int = 0, group=None, **kw):
     """run_pipeline_budget on every rank of ``group`` (one GPU each; SURVEY
     §8(e): the pipeline's work shards as independent searches) with
-    rank-specific seeds.  The ranks cooperate: at every stage boundary and
+    rank-specific seeds; ranks > 0 polish a kicked copy of the construction
+    (different local optima).  The ranks cooperate: at every stage boundary and
     after every kick round of the tail they min-all-reduce the best makespan
     and broadcast the winner's routes (alns.sync_pool_share: lowest rank wins
     ties), and continue from the global best; a final exchange makes the
@@ -264,7 +278,8 @@ def run_pipeline_budget_distributed(instance, seconds: float, seed: int = 0, gro
         dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
         return share.best_z, share.best_sol, bool(flag.item())
 
-    sol, z, trace = run_pipeline_budget(instance, seconds, seed=seed + 1009 * rank, exchange=exchange, **kw)
+    sol, z, trace = run_pipeline_budget(instance, seconds, seed=seed + 1009 * rank, exchange=exchange,
+                                        diversify=rank, **kw)
     share = A._PoolShare()
     share.offer(rank, z, sol)
     A.sync_pool_share(instance, share, group)
