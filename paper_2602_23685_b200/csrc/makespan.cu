@@ -111,14 +111,15 @@ __device__ __forceinline__ typename LegRaw<INTD>::T gather_leg(const DevInstance
 template <bool INTD>
 using TimeT = typename std::conditional<INTD, long long, double>::type;
 
-template <typename OpT, bool INTD>
+template <typename OpT, bool INTD, int OA = OPS_AHEAD, int LA = LEGS_AHEAD>
 struct RouteStream {
+    static constexpr int OPS = OA, LEGS = LA;
     using LT = typename LegRaw<INTD>::T;
     using TT = TimeT<INTD>;
     const OpT *rp;
     int L, i, two_n, lastp;
-    int o[OPS_AHEAD];
-    LT l[LEGS_AHEAD];
+    int o[OA];
+    LT l[LA];
     bool bad;
 
     // Loads never feed a select: positions past the end re-read the last op
@@ -139,22 +140,22 @@ struct RouteStream {
         rp = route; L = len; i = 0; two_n = n2; bad = false;
         lastp = len > 0 ? len - 1 : 0;  // len == 0: rp points inside the row, never consumed
 #pragma unroll
-        for (int q = 0; q < OPS_AHEAD; ++q) o[q] = fetch(q);
+        for (int q = 0; q < OA; ++q) o[q] = fetch(q);
 #pragma unroll
-        for (int q = 0; q < LEGS_AHEAD; ++q) o[q] = checked(o[q], q);
+        for (int q = 0; q < LA; ++q) o[q] = checked(o[q], q);
         l[0] = leg(I, -1, o[0]);
 #pragma unroll
-        for (int q = 1; q < LEGS_AHEAD; ++q) l[q] = leg(I, o[q - 1], o[q]);
+        for (int q = 1; q < LA; ++q) l[q] = leg(I, o[q - 1], o[q]);
     }
     __device__ __forceinline__ void advance(const DevInstance &I) {
         ++i;
 #pragma unroll
-        for (int q = 0; q + 1 < OPS_AHEAD; ++q) o[q] = o[q + 1];
-        o[OPS_AHEAD - 1] = fetch(i + OPS_AHEAD - 1);
-        o[LEGS_AHEAD - 1] = checked(o[LEGS_AHEAD - 1], i + LEGS_AHEAD - 1);
+        for (int q = 0; q + 1 < OA; ++q) o[q] = o[q + 1];
+        o[OA - 1] = fetch(i + OA - 1);
+        o[LA - 1] = checked(o[LA - 1], i + LA - 1);
 #pragma unroll
-        for (int q = 0; q + 1 < LEGS_AHEAD; ++q) l[q] = l[q + 1];
-        l[LEGS_AHEAD - 1] = leg(I, o[LEGS_AHEAD - 2], o[LEGS_AHEAD - 1]);
+        for (int q = 0; q + 1 < LA; ++q) l[q] = l[q + 1];
+        l[LA - 1] = leg(I, o[LA - 2], o[LA - 1]);
     }
     // re-read and validate the op at `pos` (capacity scan past a deadlock)
     __device__ __forceinline__ int checked_at(int pos) { return checked(fetch(pos), pos); }
@@ -530,6 +531,258 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Thread-per-candidate exact replay (integral instances, m = M fixed, m*k <=
+// SLOTS) -- the round-2 A/B against the lockstep warp replay above, compiled
+// out (VRP_K1_SERIAL=0): bit-exact (the parity suite passes with it) but
+// 20.6 M evals/s against 44.5 M at n = 999.  The per-candidate slot table
+// (1.1 KB of shared memory per thread) caps residency at 6 warps/SM, and
+// advancing one of six register-resident route pipelines without branching
+// costs ~150 instructions per route-round in register moves and selects
+// (13.5 k warp instructions per evaluation, IPC 0.91; DESIGN.md §3 K1).
+//
+// One thread owns one candidate and all M of its routes; each round visits
+// the routes in order 0..M-1 and executes the next op of each that can go.
+// Everything the lockstep warp replay spends on lane coordination -- ballots,
+// the slot-mask rotation OR, shuffles, __syncwarp per round -- disappears:
+// the free-slot mask is one register of the thread, and a dropoff executed on
+// route v is visible to a pickup on route w > v in the same round (program
+// order), so rounds <= the lockstep's DAG depth.  Results depend only on the
+// precedence DAG (every value is a max-plus function of its predecessors), so
+// they equal the reference's round-robin replay (schedule.py:265-316).
+//
+// The M route streams (op codes OA ahead, L2 leg gathers LA ahead) live in
+// registers (full unroll over the compile-time fleet); shared memory holds the
+// candidate's slot table: a u8 slot id per customer (0xFF = not dropped, 0xFE
+// = already picked up) and SLOTS uint32 ready values, laid out so that the 32
+// threads of a warp always hit 32 distinct banks (word index = x * 32 + lane).
+// Event times are uint32; a wrap, an exhausted slot mask (capacity-infeasible
+// by the conservation argument above) or a second pickup of one customer send
+// the candidate to the 64-bit fix-up pass (ST_RETRY), so results stay exact.
+// predicated loads: the replay advances a route only when its op executes,
+// without branching the warp
+__device__ __forceinline__ int ldg_if(const int16_t *p, bool pr, int old) {
+    int r = old;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.s16 %0, [%1];\n\t}"
+                 : "+r"(r) : "l"(p), "r"((int)pr));
+    return r;
+}
+__device__ __forceinline__ int ldg_if(const int32_t *p, bool pr, int old) {
+    int r = old;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.b32 %0, [%1];\n\t}"
+                 : "+r"(r) : "l"(p), "r"((int)pr));
+    return r;
+}
+__device__ __forceinline__ int ldcg_if(const int32_t *p, bool pr, int old) {
+    int r = old;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.cg.b32 %0, [%1];\n\t}"
+                 : "+r"(r) : "l"(p), "r"((int)pr));
+    return r;
+}
+
+// One route of the thread-per-candidate replay: op codes OA ahead, and at the
+// gather stage (LA-1) the leg d[prev][c] from L2 plus p[c] (used by dropoffs),
+// so nothing the replay reads at stage 0 is a fresh load.  advance_if(go)
+// moves the pipeline only when go (selects + predicated loads, no branch).
+template <typename OpT, int OA, int LA>
+struct SerialRoute {
+    const OpT *rp;
+    int L, i, lastp, two_n;
+    bool bad;
+    int o[OA];
+    int32_t l[LA], pp[LA];
+
+    __device__ __forceinline__ const OpT *at(int pos) const { return rp + (pos < L ? pos : lastp); }
+    __device__ __forceinline__ int checked(int op, int pos) {
+        if (pos >= L) return -1;
+        if ((unsigned)op >= (unsigned)two_n) { bad = true; return 0; }
+        return op;
+    }
+    __device__ __forceinline__ uint32_t gidx(const DevInstance &I, int prev_op, int op) const {
+        const int a = prev_op < 0 ? 0 : op_customer(prev_op);
+        return (uint32_t)a * (uint32_t)I.W + (uint32_t)op_customer(op < 0 ? 0 : op);
+    }
+    __device__ __forceinline__ void init(const DevInstance &I, const OpT *route, int len, int n2) {
+        rp = route; L = len; i = 0; two_n = n2; bad = false;
+        lastp = len > 0 ? len - 1 : 0;
+#pragma unroll
+        for (int q = 0; q < OA; ++q) o[q] = (int)__ldg(at(q));
+#pragma unroll
+        for (int q = 0; q < LA; ++q) o[q] = checked(o[q], q);
+#pragma unroll
+        for (int q = 0; q < LA; ++q) {
+            l[q] = o[q] < 0 ? 0 : __ldcg(I.d32 + gidx(I, q ? o[q - 1] : -1, o[q]));
+            pp[q] = __ldg(I.p32 + op_customer(o[q] < 0 ? 0 : o[q]));
+        }
+    }
+    __device__ __forceinline__ void advance_if(const DevInstance &I, bool go) {
+        i += go ? 1 : 0;
+#pragma unroll
+        for (int q = 0; q + 1 < OA; ++q) o[q] = go ? o[q + 1] : o[q];
+        o[OA - 1] = ldg_if(at(i + OA - 1), go, o[OA - 1]);
+        const int h = checked(o[LA - 1], i + LA - 1);  // o[LA-1] was raw (one stage behind)
+        o[LA - 1] = go ? h : o[LA - 1];
+#pragma unroll
+        for (int q = 0; q + 1 < LA; ++q) { l[q] = go ? l[q + 1] : l[q]; pp[q] = go ? pp[q + 1] : pp[q]; }
+        const bool g2 = go && h >= 0;
+        l[LA - 1] = ldcg_if(I.d32 + gidx(I, o[LA - 2], h), g2, go ? 0 : l[LA - 1]);
+        pp[LA - 1] = ldg_if(I.p32 + op_customer(h < 0 ? 0 : h), g2, pp[LA - 1]);
+    }
+};
+
+template <typename OpT, int M, int OA, int LA>
+__global__ void __launch_bounds__(32)
+serial_exact_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
+                    const int32_t *__restrict__ lens, int64_t N, double *__restrict__ z_out,
+                    int32_t *__restrict__ status_out, double *__restrict__ returns_out,
+                    int32_t *__restrict__ bottleneck_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x;
+    const int n = I.n, k = I.k, two_n = 2 * n;
+    const int mwords = (n + 4) >> 2;  // slot ids of customers 0..n, 4 per word
+    unsigned char *s_map = smem + lane * 4;  // customer c: byte (c & ~3) * 32 + (c & 3)
+    uint32_t *s_mapw = reinterpret_cast<uint32_t *>(smem) + lane;
+    // slot q: [q * 32]; slot SLOTS is a scratch target for the unconditional store
+    uint32_t *s_val = reinterpret_cast<uint32_t *>(smem + (size_t)mwords * 128) + lane;
+
+    for (int64_t base = (int64_t)blockIdx.x * 32; base < N; base += (int64_t)gridDim.x * 32) {
+        const int64_t cand = base + lane;
+        const bool live = cand < N;
+        int L[M], off[M];
+        int total = 0;
+        bool mal = false;
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+            const int x = live ? __ldg(lens + cand * M + v) : 0;
+            mal |= x < 0;
+            L[v] = x;
+            off[v] = total;
+            total += x;
+        }
+        mal |= total > two_n || total > stride;
+        const bool run = live && !mal;
+        const OpT *row = ops + (run ? cand : 0) * stride;
+        SerialRoute<OpT, OA, LA> rs[M];
+#pragma unroll
+        for (int v = 0; v < M; ++v) rs[v].init(I, row + (run && L[v] > 0 ? off[v] : 0), run ? L[v] : 0, two_n);
+        for (int w = 0; w < mwords; ++w) s_mapw[w * 32] = 0xFFFFFFFFu;
+
+        uint32_t t[M];
+        int lastc[M], sc[M], lo[M], hi[M];
+#pragma unroll
+        for (int v = 0; v < M; ++v) { t[v] = 0; lastc[v] = 0; sc[v] = 0; lo[v] = 0; hi[v] = k; }
+        uint32_t freem = ~0u;
+        bool dead = false, ovf = false;
+        if (run) {
+            for (;;) {
+                bool moved = false, left = false;
+#pragma unroll
+                for (int v = 0; v < M; ++v) {
+                    const bool act = rs[v].i < rs[v].L;
+                    const int op = rs[v].o[0];  // -1 past the end: customer 0 (unused map entry)
+                    const int c = op_customer(op);
+                    const bool pick = op & 1;
+                    unsigned char *mp = s_map + ((c & ~3) << 5) + (c & 3);
+                    const int sid = *mp;
+                    const uint32_t r = s_val[(sid & (SLOTS - 1)) * 32];
+                    const uint32_t arr = t[v] + (uint32_t)rs[v].l[0];
+                    const int slot = __ffs(freem) - 1;
+                    const bool go = act && (!pick || sid < SLOTS);
+                    const uint32_t rv = arr + (uint32_t)rs[v].pp[0];
+                    ovf |= act && (arr < t[v] || (pick ? sid == 0xFE : (slot < 0 || rv < arr)));
+                    const uint32_t tn = (pick && r > arr) ? r : arr;
+                    const bool dgo = go && !pick;
+                    s_val[((dgo && slot >= 0) ? slot : SLOTS) * 32] = rv;
+                    *mp = (unsigned char)(go ? (pick ? 0xFE : slot) : sid);
+                    freem = go ? (pick ? (freem | (1u << (sid & (SLOTS - 1)))) : (freem & (freem - 1))) : freem;
+                    t[v] = go ? tn : t[v];
+                    lastc[v] = go ? c : lastc[v];
+                    const int room = k - 1 - sc[v], need = 1 - sc[v];
+                    hi[v] = (go && pick && room < hi[v]) ? room : hi[v];
+                    lo[v] = (dgo && need > lo[v]) ? need : lo[v];
+                    sc[v] += go ? (pick ? 1 : -1) : 0;
+                    rs[v].advance_if(I, go);
+                    moved |= go;
+                    left |= rs[v].i < rs[v].L;
+                }
+                if (!left || ovf) break;
+                if (!moved) { dead = true; break; }
+            }
+        }
+        bool bad = false, capfail = false;
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+            if (dead)  // finish the capacity test past the stuck position
+                for (int j = rs[v].i; j < rs[v].L; ++j)
+                    cap_step(rs[v].checked((int)__ldg(rs[v].at(j)), j), k, sc[v], lo[v], hi[v]);
+            bad |= rs[v].bad;
+            capfail |= lo[v] > hi[v];
+        }
+        mal |= bad;
+        const int st = mal ? ST_MAL : (ovf ? ST_RETRY : (capfail ? ST_CAP : (dead ? ST_DEAD : ST_OK)));
+        double ret[M], z = 0.0;
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+            ret[v] = 0.0;
+            if (live && st == ST_OK && L[v] > 0)
+                ret[v] = (double)((long long)t[v] + (long long)__ldg(I.d32 + (int64_t)lastc[v] * I.W));
+            z = ret[v] > z ? ret[v] : z;
+        }
+        if (live) {
+            int bn = 0;
+#pragma unroll
+            for (int v = M - 1; v >= 0; --v) bn = ret[v] == z ? v : bn;
+            z_out[cand] = st == ST_OK ? z : 0.0;
+            status_out[cand] = st;
+            if (bottleneck_out) bottleneck_out[cand] = bn;
+            if (returns_out)
+#pragma unroll
+                for (int v = 0; v < M; ++v) returns_out[cand * M + v] = ret[v];
+        }
+    }
+}
+
+#ifndef VRP_K1_SERIAL
+#define VRP_K1_SERIAL 0  // thread-per-candidate exact replay; measured slower, see DESIGN.md
+#endif
+#ifndef VRP_K1S_OA
+#define VRP_K1S_OA 8
+#endif
+#ifndef VRP_K1S_LA
+#define VRP_K1S_LA 4
+#endif
+
+struct SerialShape {
+    int blocks;
+    size_t smem;
+};
+
+template <typename OpT, int M>
+int launch_serial(const DevInstance &I, const void *ops, int64_t stride, const int32_t *lens, int64_t N,
+                  double *z, int32_t *status, double *returns, int32_t *bottleneck, cudaStream_t stream,
+                  int sm_count) {
+    auto kern = serial_exact_kernel<OpT, M, VRP_K1S_OA, VRP_K1S_LA>;
+    static PlanCache<SerialShape> cache;
+    SerialShape sh;
+    const int rc = cache.get(I.n, sh, [&](SerialShape &out) {
+        out.smem = (size_t)((I.n + 4) >> 2) * 128 + (size_t)(SLOTS + 1) * 128;
+        if (out.smem > 227 * 1024) return -2;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)out.smem) != cudaSuccess)
+            return -1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&out.blocks, kern, 32, out.smem) != cudaSuccess)
+            return -1;
+        return out.blocks > 0 ? 0 : -2;
+    });
+    if (rc) return rc;
+    int64_t grid = (int64_t)sh.blocks * sm_count;
+    const int64_t want = (N + 31) / 32;
+    if (grid > want) grid = want;
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, 32, sh.smem, stream>>>(I, static_cast<const OpT *>(ops), stride, lens, N, z, status,
+                                                   returns, bottleneck);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
+}
+
 // (candidates per warp, warps per block) maximising resident candidates per SM
 struct Shape {
     int G, wpb, blocks;
@@ -590,8 +843,16 @@ template <typename OpT, int MODE>
 int launch_narrow(const DevInstance &I, const void *ops, int64_t stride, const int32_t *lens,
                   int64_t N, double *z, int32_t *status, double *returns, int32_t *bottleneck,
                   cudaStream_t stream, int sm_count) {
-    int rc;
-    if (MODE != MODE_TWO && I.m == 6 && I.k <= SLOTS / 6)  // slot table, m fixed at 6 (+ run-ahead: exact)
+    int rc = -1;
+    bool done = false;
+    if constexpr (VRP_K1_SERIAL != 0 && MODE == MODE_EXACT) {  // thread per candidate (A/B, compiled out)
+        if (I.m == 6 && I.k <= SLOTS / 6) {
+            rc = launch_serial<OpT, 6>(I, ops, stride, lens, N, z, status, returns, bottleneck, stream, sm_count);
+            done = true;
+        }
+    }
+    if (done) {
+    } else if (MODE != MODE_TWO && I.m == 6 && I.k <= SLOTS / 6)  // slot table, m fixed at 6 (+ run-ahead: exact)
         rc = launch_t<OpT, true, MODE, false, true, true, 6, MODE == MODE_EXACT ? VRP_K1_RA : 0>(
             I, ops, stride, lens, N, z, status, returns, bottleneck, nullptr, nullptr, nullptr, stream, sm_count, 0);
     else if (MODE != MODE_TWO && I.m * I.k <= SLOTS)  // slot table (see makespan_kernel: COMPACT)
