@@ -210,6 +210,23 @@ int vrp_ls_build(vrp_instance_t h, int32_t kind, const int32_t *base_ops, const 
  * x, y: n DEVICE doubles. */
 int vrp_sa_exp(const double *x, double *y, int64_t n, void *stream);
 
+/* The local-search neighbourhood entries of W solutions, built on the device
+ * from their evaluate returns (alns.py:416-450 pickup_repositioning, kind 0;
+ * :453-487 cross_agent_relocation, kind 1), in the reference's generation
+ * order, in the layout vrp_ls_build consumes:
+ *   kind 0: solutions with z > 0, vehicles with return >= 0.9 z, each pickup
+ *     in route order -> {w, v, i, flat, 0}, 2n + m - 2 candidates each
+ *   kind 1: b = first argmax of the returns, customers of route b ascending,
+ *     every vehicle u != b -> {w, c, u, f1, f2}, (L+1)(L+2)/2 candidates
+ *   base_ops[W][2n], base_lens[W][m], z[W], returns[W][m], active[W] (u8) DEVICE
+ * Two calls: count phase (entry_off = cand_off = NULL) writes entry_count[W]
+ * and cand_count[W]; the fill phase, given their exclusive prefix sums
+ * entry_off[W] / cand_off[W], writes entries[E][5] and entry_start[E]. */
+int vrp_ls_entries(vrp_instance_t h, int32_t kind, const int32_t *base_ops, const int32_t *base_lens,
+                   const double *z, const double *returns, const uint8_t *active, int32_t W,
+                   const int64_t *entry_off, const int64_t *cand_off, int32_t *entry_count, int64_t *cand_count,
+                   int32_t *entries, int64_t *entry_start, void *stream);
+
 /* The verification shortlist of the batched local search (alns.py:401-413:
  * stable sort of the survivors by estimate, first _VERIFY_LIMIT), per solution,
  * over a chunk of estimated candidates: candidates with status 0 and

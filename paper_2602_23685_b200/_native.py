@@ -96,8 +96,10 @@ def declare_k4(L):
     L.vrp_sa_exp.argtypes = [P, P, i64, P]
     L.vrp_remove_batch.argtypes = [P, P, i64, P, P, i64, P, P, i64, P, P, i64, P, i64, P]
     L.vrp_removal_gains.argtypes = [P, P, i64, P, P, i64, i64, P]
+    L.vrp_ls_entries.argtypes = [P, C.c_int32, P, P, P, P, P, C.c_int32, P, P, P, P, P, P, P]
     L.vrp_ls_topk.argtypes = [P, P, i64, P, P, P, P, i64, P, P, P, C.c_int32, C.c_int32, P, P, P, P]
     for name in ("vrp_fitness_order", "vrp_evolve", "vrp_best_update", "vrp_repair_batch",
                  "vrp_destroy_batch", "vrp_alns_iterate", "vrp_ls_build", "vrp_random_fill",
-                 "vrp_sa_exp", "vrp_remove_batch", "vrp_removal_gains", "vrp_ls_topk"):
+                 "vrp_sa_exp", "vrp_remove_batch", "vrp_removal_gains", "vrp_ls_topk",
+                 "vrp_ls_entries"):
         getattr(L, name).restype = C.c_int

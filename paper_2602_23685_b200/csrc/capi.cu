@@ -355,6 +355,29 @@ int vrp_ls_build(vrp_instance_t h, int32_t kind, const int32_t *base_ops, const 
                          "vrp_ls_build");
 }
 
+int vrp_ls_entries(vrp_instance_t h, int32_t kind, const int32_t *base_ops, const int32_t *base_lens,
+                   const double *z, const double *returns, const uint8_t *active, int32_t W,
+                   const int64_t *entry_off, const int64_t *cand_off, int32_t *entry_count, int64_t *cand_count,
+                   int32_t *entries, int64_t *entry_start, void *stream) {
+    if (!h) return fail(VRP_EINVAL, "null instance%s");
+    DeviceGuard dg(h->device);
+    if (kind != 0 && kind != 1) return fail(VRP_EINVAL, "vrp_ls_entries: kind must be 0 or 1%s");
+    if (W < 0) return fail(VRP_EINVAL, "vrp_ls_entries: W < 0%s");
+    if (W == 0) return 0;
+    if (!base_ops || !base_lens || !z || !returns || !active)
+        return fail(VRP_EINVAL, "vrp_ls_entries: null buffer%s");
+    if ((entry_off == nullptr) != (cand_off == nullptr) ||
+        (entry_off ? (!entries || !entry_start) : (!entry_count || !cand_count)))
+        return fail(VRP_EINVAL, "vrp_ls_entries: count phase needs entry_count/cand_count, fill phase "
+                                "entry_off/cand_off/entries/entry_start%s");
+    if (kind == 1 && 8 * ((int64_t)h->dev.n + 1) > 227 * 1024)
+        return fail(VRP_EUNSUPPORTED, "vrp_ls_entries: cross entries need 8 (n + 1) bytes of shared memory%s");
+    return launch_result(launch_ls_entries(kind, h->dev.n, h->dev.m, base_ops, base_lens, z, returns, active, W,
+                                           entry_off, cand_off, entry_count, cand_count, entries, entry_start,
+                                           static_cast<cudaStream_t>(stream)),
+                         "vrp_ls_entries");
+}
+
 int vrp_ls_topk(const double *z, const int32_t *status, int64_t first, const double *zthr,
                 const int32_t *seg_worker, const int64_t *seg_begin, const int64_t *seg_end, int64_t nseg,
                 const int32_t *workers, const int32_t *wseg_first, const int32_t *wseg_count, int32_t nworkers,

@@ -58,6 +58,10 @@ int launch_ls_build(int kind, int n, int m, const int32_t *base_ops, const int32
                     const int32_t *entries, const int64_t *entry_start, int64_t n_entries,
                     const int64_t *index_list, int64_t first, int64_t count, void *out_ops, int op_bytes,
                     int32_t *out_lens, cudaStream_t stream);
+int launch_ls_entries(int kind, int n, int m, const int32_t *base_ops, const int32_t *base_lens, const double *z,
+                      const double *returns, const uint8_t *active, int32_t W, const int64_t *entry_off,
+                      const int64_t *cand_off, int32_t *entry_count, int64_t *cand_count, int32_t *entries,
+                      int64_t *entry_start, cudaStream_t stream);
 int launch_ls_topk(const double *z, const int32_t *status, int64_t first, const double *zthr,
                    const int32_t *seg_worker, const int64_t *seg_begin, const int64_t *seg_end, int64_t nseg,
                    const int32_t *workers, const int32_t *wseg_first, const int32_t *wseg_count, int32_t nworkers,

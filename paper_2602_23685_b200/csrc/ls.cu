@@ -256,6 +256,125 @@ ls_merge_topk_kernel(const int32_t *__restrict__ workers, const int32_t *__restr
     }
 }
 
+// ---- the neighbourhood entries of every solution, built on the device from
+// the evaluate returns (alns.py:416-487's generation order), so the local
+// search never copies solutions back to the host.  Block (one warp) per
+// solution; count phase (eoff == null): entries and candidates per solution;
+// fill phase: entries[e] and entry_start[e] at the host-scanned offsets.
+//   kind 0 (pickup_repositioning, :416-450): solutions with z > 0, vehicles
+//     whose return >= 0.9 z, every pickup in route order:
+//     {w, v, i, flat, 0}, 2n + m - 2 candidates each
+//   kind 1 (cross_agent_relocation, :453-487): b = first argmax of the
+//     returns; customers of route b ascending; every other vehicle u:
+//     {w, c, u, f1, f2} (f1 < f2: c's flat positions), (L+1)(L+2)/2
+//     candidates, L = route u's length without c's ops
+__global__ void __launch_bounds__(32)
+ls_entries_kernel(int kind, int n, int m, const int32_t *__restrict__ base_ops, const int32_t *__restrict__ base_lens,
+                  const double *__restrict__ z, const double *__restrict__ returns,
+                  const uint8_t *__restrict__ active, const int64_t *__restrict__ eoff,
+                  const int64_t *__restrict__ coff, int32_t *__restrict__ ecount, int64_t *__restrict__ ccount,
+                  int32_t *__restrict__ entries, int64_t *__restrict__ starts) {
+    extern __shared__ int32_t s_first[];  // kind 1: first / second flat position of each customer
+    const int w = blockIdx.x, lane = threadIdx.x, n2 = 2 * n;
+    const int32_t *ops = base_ops + (int64_t)w * n2;
+    const int32_t *lens = base_lens + (int64_t)w * m;
+    const double *ret = returns + (int64_t)w * m;
+    const bool fill = eoff != nullptr;
+    const int64_t e0 = fill ? eoff[w] : 0, c0 = fill ? coff[w] : 0;
+    int ne = 0;
+    int64_t nc = 0;
+    if (active[w] && kind == 0) {
+        const double zw = z[w];
+        if (!(zw <= 0.0)) {
+            const int64_t K = n2 + m - 2;
+            int off = 0;
+            for (int v = 0; v < m; ++v) {
+                const int Lv = lens[v];
+                if (ret[v] >= 0.9 * zw) {
+                    for (int b = 0; b < Lv; b += 32) {
+                        const int i = b + lane;
+                        const bool pk = i < Lv && (ops[off + i] & 1);
+                        const unsigned bal = __ballot_sync(VRP_FULL_MASK, pk);
+                        if (fill && pk) {
+                            const int64_t r = ne + __popc(bal & lanemask_lt());
+                            int32_t *E = entries + (e0 + r) * 5;
+                            E[0] = w; E[1] = v; E[2] = i; E[3] = off + i; E[4] = 0;
+                            starts[e0 + r] = c0 + r * K;
+                        }
+                        ne += __popc(bal);
+                    }
+                }
+                off += Lv;
+            }
+            nc = (int64_t)ne * K;
+        }
+    } else if (active[w] && kind == 1 && m > 1) {
+        int b = 0;
+        for (int v = 1; v < m; ++v) b = ret[v] > ret[b] ? v : b;  // np.argmax: first maximum
+        int offb = 0, total = 0;
+        for (int v = 0; v < m; ++v) {
+            if (v < b) offb += lens[v];
+            total += lens[v];
+        }
+        const int Lb = lens[b];
+        int32_t *f1 = s_first, *f2 = s_first + n + 1;
+        for (int c = lane; c <= n; c += 32) { f1[c] = INT32_MAX; f2[c] = INT32_MAX; }
+        __syncwarp();
+        for (int q = lane; q < total; q += 32) atomicMin(&f1[op_customer(ops[q])], q);
+        __syncwarp();
+        for (int q = lane; q < total; q += 32) {
+            const int c = op_customer(ops[q]);
+            if (q != f1[c]) atomicMin(&f2[c], q);
+        }
+        __syncwarp();
+        for (int cb = 1; cb <= n; cb += 32) {
+            const int c = cb + lane;
+            const int p1 = c <= n ? f1[c] : INT32_MAX, p2 = c <= n ? f2[c] : INT32_MAX;
+            const bool onb = (p1 >= offb && p1 < offb + Lb) || (p2 >= offb && p2 < offb + Lb);
+            const unsigned bal = __ballot_sync(VRP_FULL_MASK, onb);
+            if (!bal) continue;
+            int64_t mine = 0;
+            if (onb) {
+                int off = 0;
+                for (int u = 0; u < m; ++u) {
+                    const int Lu = lens[u];
+                    if (u != b) {
+                        const int L = Lu - (p1 >= off && p1 < off + Lu) - (p2 >= off && p2 < off + Lu);
+                        mine += (int64_t)(L + 1) * (L + 2) / 2;
+                    }
+                    off += Lu;
+                }
+            }
+            int64_t incl = mine;  // inclusive scan over the lanes (customer order)
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t y = __shfl_up_sync(VRP_FULL_MASK, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (fill && onb) {
+                int64_t r = ne + (int64_t)__popc(bal & lanemask_lt()) * (m - 1);
+                int64_t st = c0 + nc + incl - mine;
+                int off = 0;
+                for (int u = 0; u < m; ++u) {
+                    const int Lu = lens[u];
+                    if (u != b) {
+                        const int L = Lu - (p1 >= off && p1 < off + Lu) - (p2 >= off && p2 < off + Lu);
+                        int32_t *E = entries + (e0 + r) * 5;
+                        E[0] = w; E[1] = c; E[2] = u; E[3] = p1; E[4] = p2;
+                        starts[e0 + r] = st;
+                        st += (int64_t)(L + 1) * (L + 2) / 2;
+                        ++r;
+                    }
+                    off += Lu;
+                }
+            }
+            ne += __popc(bal) * (m - 1);
+            nc += __shfl_sync(VRP_FULL_MASK, incl, 31);
+        }
+    }
+    if (!fill && lane == 0) { ecount[w] = ne; ccount[w] = nc; }
+}
+
 }  // namespace
 
 int launch_ls_build(int kind, int n, int m, const int32_t *base_ops, const int32_t *base_lens,
@@ -300,4 +419,19 @@ int launch_ls_topk(const double *z, const int32_t *status, int64_t first, const 
     cudaFreeAsync(si, stream);
     cudaFreeAsync(sn, stream);
     return e == cudaSuccess ? 0 : -1;
+}
+
+int launch_ls_entries(int kind, int n, int m, const int32_t *base_ops, const int32_t *base_lens, const double *z,
+                      const double *returns, const uint8_t *active, int32_t W, const int64_t *entry_off,
+                      const int64_t *cand_off, int32_t *entry_count, int64_t *cand_count, int32_t *entries,
+                      int64_t *entry_start, cudaStream_t stream) {
+    if (W <= 0) return 0;
+    const size_t smem = kind == 1 ? sizeof(int32_t) * 2 * (size_t)(n + 1) : 0;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(ls_entries_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return -1;
+    ls_entries_kernel<<<(unsigned)W, 32, smem, stream>>>(kind, n, m, base_ops, base_lens, z, returns, active,
+                                                          entry_off, cand_off, entry_count, cand_count, entries,
+                                                          entry_start);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
 }

@@ -113,7 +113,6 @@ using TimeT = typename std::conditional<INTD, long long, double>::type;
 
 template <typename OpT, bool INTD, int OA = OPS_AHEAD, int LA = LEGS_AHEAD>
 struct RouteStream {
-    static constexpr int OPS = OA, LEGS = LA;
     using LT = typename LegRaw<INTD>::T;
     using TT = TimeT<INTD>;
     const OpT *rp;
@@ -531,6 +530,10 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     }
 }
 
+#ifndef VRP_K1_SERIAL
+#define VRP_K1_SERIAL 0  // thread-per-candidate exact replay; measured slower, see DESIGN.md
+#endif
+#if VRP_K1_SERIAL
 // ---------------------------------------------------------------------------
 // Thread-per-candidate exact replay (integral instances, m = M fixed, m*k <=
 // SLOTS) -- the round-2 A/B against the lockstep warp replay above, compiled
@@ -742,9 +745,6 @@ serial_exact_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
     }
 }
 
-#ifndef VRP_K1_SERIAL
-#define VRP_K1_SERIAL 0  // thread-per-candidate exact replay; measured slower, see DESIGN.md
-#endif
 #ifndef VRP_K1S_OA
 #define VRP_K1S_OA 8
 #endif
@@ -782,6 +782,8 @@ int launch_serial(const DevInstance &I, const void *ops, int64_t stride, const i
                                                    returns, bottleneck);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -1;
 }
+
+#endif  // VRP_K1_SERIAL
 
 // (candidates per warp, warps per block) maximising resident candidates per SM
 struct Shape {
@@ -845,12 +847,12 @@ int launch_narrow(const DevInstance &I, const void *ops, int64_t stride, const i
                   cudaStream_t stream, int sm_count) {
     int rc = -1;
     bool done = false;
-    if constexpr (VRP_K1_SERIAL != 0 && MODE == MODE_EXACT) {  // thread per candidate (A/B, compiled out)
-        if (I.m == 6 && I.k <= SLOTS / 6) {
-            rc = launch_serial<OpT, 6>(I, ops, stride, lens, N, z, status, returns, bottleneck, stream, sm_count);
-            done = true;
-        }
+#if VRP_K1_SERIAL
+    if (MODE == MODE_EXACT && I.m == 6 && I.k <= SLOTS / 6) {  // thread per candidate (A/B, compiled out)
+        rc = launch_serial<OpT, 6>(I, ops, stride, lens, N, z, status, returns, bottleneck, stream, sm_count);
+        done = true;
     }
+#endif
     if (done) {
     } else if (MODE != MODE_TWO && I.m == 6 && I.k <= SLOTS / 6)  // slot table, m fixed at 6 (+ run-ahead: exact)
         rc = launch_t<OpT, true, MODE, false, true, true, 6, MODE == MODE_EXACT ? VRP_K1_RA : 0>(

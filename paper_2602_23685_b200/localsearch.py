@@ -5,9 +5,11 @@ many solutions at once.
 Each improvement pass of every solution is:
   1. K1 ``evaluate`` of the current solutions (returns -> hot vehicles / the
      bottleneck), one launch for all of them;
-  2. the neighbourhood, numbered in the reference's generation order, built
-     chunk by chunk on the device (``vrp_ls_build``) and estimated by K2
-     ``two_pass_estimate`` -- nothing is materialised on the host;
+  2. the neighbourhood entries built on the device from those returns
+     (``vrp_ls_entries``: a count launch, the host scans W counts, a fill
+     launch), then the candidates, numbered in the reference's generation
+     order, built chunk by chunk (``vrp_ls_build``) and estimated by K2
+     ``two_pass_estimate`` -- solutions never leave the device;
   3. survivors (status 0, estimate < z - 1e-9) reduced on the device to each
      solution's ten best by (estimate, generation index) -- the reference's
      stable sort + ``[:_VERIFY_LIMIT]`` -- by ``vrp_ls_topk`` (per-segment
@@ -63,23 +65,19 @@ def _segments(wid, wb, we, first, cnt):
     return seg_w, seg_b.astype(np.int64), seg_e.astype(np.int64), wid.astype(np.int32), wfirst, nseg.astype(np.int32)
 
 
-def _search(instance, kind, ops_t, lens_t, entries, counts, z):
-    """Steps 2-4 for every worker that has entries.  Returns
+def _search(instance, kind, ops_t, lens_t, ent_t, start_t, ccount, coff, z):
+    """Steps 2-4 for the solutions that have entries (device tables ent_t /
+    start_t, per-solution candidate counts / offsets on the host).  Returns
     {worker: (z_exact, ops row, lens row)} for the workers that improved."""
     dev = ops_t.device
     n = instance.n
     W = ops_t.shape[0]
-    starts = np.zeros(len(counts), np.int64)
-    np.cumsum(counts[:-1], out=starts[1:])
-    total = int(counts.sum())
-    ent_t = torch.from_numpy(np.ascontiguousarray(entries, np.int32)).to(dev)
-    start_t = torch.from_numpy(starts).to(dev)
+    total = int(ccount.sum())
     zthr = torch.from_numpy(np.asarray(z, np.float64) - 1e-9).to(dev)
     # each solution's candidates are one contiguous range (entries are grouped by solution)
-    ew = np.asarray(entries, np.int64)[:, 0]
-    wid, pos = np.unique(ew, return_index=True)
-    last = np.r_[pos[1:], ew.size] - 1
-    wb, we = starts[pos], starts[last] + counts[last]
+    wid = np.flatnonzero(ccount > 0)
+    wb = coff[wid]
+    we = wb + ccount[wid]
     # running lists: only the first top_n entries are ever read (no fill kernels)
     top_z = torch.empty((W, VERIFY_LIMIT), dtype=torch.float64, device=dev)
     top_i = torch.empty((W, VERIFY_LIMIT), dtype=torch.int64, device=dev)
@@ -122,43 +120,38 @@ def _evaluate(instance, ops_t, lens_t):
     return r["z"].cpu().numpy(), r["returns"].cpu().numpy()
 
 
-def _pickup_entries(ops, lens, z, returns, active):
-    m = lens.shape[1]
-    ent, alive = [], []
-    for w in active:
-        if z[w] <= 0:
-            continue
-        alive.append(w)
-        off = np.concatenate([[0], np.cumsum(lens[w])[:-1]])
-        for v in range(m):
-            if not returns[w, v] >= NEAR_BOTTLENECK * z[w]:
-                continue
-            seg = ops[w, off[v]:off[v] + lens[w, v]]
-            for i in np.flatnonzero(seg & 1):
-                ent.append((w, v, int(i), int(off[v] + i), 0))
-    return ent, alive
-
-
-def _cross_entries(ops, lens, z, returns, active):
-    m = lens.shape[1]
-    ent, cnt = [], []
-    for w in active:
-        b = int(np.argmax(returns[w]))  # Schedule.bottleneck: first max
-        off = np.concatenate([[0], np.cumsum(lens[w])[:-1]])
-        total = int(lens[w].sum())
-        flat = ops[w, :total]
-        cust = (flat >> 1) + 1
-        route = np.repeat(np.arange(m), lens[w])
-        for c in sorted(set(cust[off[b]:off[b] + lens[w, b]].tolist())):
-            pos = np.flatnonzero(cust == c)
-            f1, f2 = int(pos[0]), int(pos[1])
-            for u in range(m):
-                if u == b:
-                    continue
-                L = int(lens[w, u]) - int((route[pos] == u).sum())
-                ent.append((w, c, u, f1, f2))
-                cnt.append((L + 1) * (L + 2) // 2)
-    return ent, np.asarray(cnt, np.int64)
+def entries(instance, kind, ops_t, lens_t, z, returns, active):
+    """The pass's neighbourhood entries, built on the device (vrp_ls_entries).
+    z [W] / returns [W, m] host arrays, active: worker indices.  Returns
+    (entries int32 [E, 5] device, entry_start int64 [E] device, per-solution
+    candidate counts and offsets (numpy int64 [W]))."""
+    dev = ops_t.device
+    di = DV.device_instance(instance)
+    W = ops_t.shape[0]
+    act = np.zeros(W, np.uint8)
+    act[np.asarray(list(active), np.int64)] = 1
+    z_t = torch.from_numpy(np.ascontiguousarray(z, np.float64)).to(dev)
+    r_t = torch.from_numpy(np.ascontiguousarray(returns, np.float64)).to(dev)
+    a_t = torch.from_numpy(act).to(dev)
+    ec = torch.empty(W, dtype=torch.int32, device=dev)
+    cc = torch.empty(W, dtype=torch.int64, device=dev)
+    L, h, s = N.lib(), di.handle, N.stream_handle()
+    N.check(L.vrp_ls_entries(h, kind, N.ptr(ops_t), N.ptr(lens_t), N.ptr(z_t), N.ptr(r_t), N.ptr(a_t), W,
+                             None, None, N.ptr(ec), N.ptr(cc), None, None, s), "vrp_ls_entries")
+    ecount, ccount = ec.cpu().numpy().astype(np.int64), cc.cpu().numpy()
+    eoff = np.zeros(W, np.int64)
+    coff = np.zeros(W, np.int64)
+    np.cumsum(ecount[:-1], out=eoff[1:])
+    np.cumsum(ccount[:-1], out=coff[1:])
+    E = int(ecount.sum())
+    ent_t = torch.empty((max(E, 1), 5), dtype=torch.int32, device=dev)
+    start_t = torch.empty(max(E, 1), dtype=torch.int64, device=dev)
+    if E:
+        eo, co = torch.from_numpy(eoff).to(dev), torch.from_numpy(coff).to(dev)
+        N.check(L.vrp_ls_entries(h, kind, N.ptr(ops_t), N.ptr(lens_t), N.ptr(z_t), N.ptr(r_t), N.ptr(a_t), W,
+                                 N.ptr(eo), N.ptr(co), None, None, N.ptr(ent_t), N.ptr(start_t), s),
+                "vrp_ls_entries")
+    return ent_t[:E], start_t[:E], ccount, coff
 
 
 def _run(instance, kind, ops, lens):
@@ -167,7 +160,7 @@ def _run(instance, kind, ops, lens):
     dev = torch.device("cuda", torch.cuda.current_device())
     ops_t = torch.as_tensor(ops, dtype=torch.int32).to(dev).contiguous().clone()
     lens_t = torch.as_tensor(lens, dtype=torch.int32).to(dev).contiguous().clone()
-    W, m, n = ops_t.shape[0], instance.m, instance.n
+    W, m = ops_t.shape[0], instance.m
     z, returns = _evaluate(instance, ops_t, lens_t)
     z_out = z.copy()
     if kind == 1 and m == 1:
@@ -176,15 +169,10 @@ def _run(instance, kind, ops, lens):
     for _ in range(PASSES):
         if not active:
             break
-        ops_np, lens_np = ops_t.cpu().numpy(), lens_t.cpu().numpy()
-        if kind == 0:
-            ent, active = _pickup_entries(ops_np, lens_np, z, returns, active)
-            counts = np.full(len(ent), 2 * n + m - 2, np.int64)
-        else:
-            ent, counts = _cross_entries(ops_np, lens_np, z, returns, active)
-        if not ent:
+        ent_t, start_t, ccount, coff = entries(instance, kind, ops_t, lens_t, z, returns, active)
+        if not ent_t.shape[0]:
             break
-        res = _search(instance, kind, ops_t, lens_t, np.asarray(ent, np.int32), counts, z)
+        res = _search(instance, kind, ops_t, lens_t, ent_t, start_t, ccount, coff, z)
         active = sorted(res)
         for w, (zb, o, l) in res.items():
             ops_t[w] = o

@@ -143,3 +143,48 @@ def cross_agent_relocation_host(instance, solution: Solution) -> Solution:
             break
         tours = new_tours
     return Solution.from_lists(tours)
+
+
+# The entry lists of one local-search pass built on the host from numpy arrays
+# (the reference's generation order, alns.py:416-487) -- the checker of the
+# device builder vrp_ls_entries (localsearch.entries).
+NEAR_BOTTLENECK = _NEAR_BOTTLENECK
+
+
+def pickup_entries(ops, lens, z, returns, active):
+    m = lens.shape[1]
+    ent, alive = [], []
+    for w in active:
+        if z[w] <= 0:
+            continue
+        alive.append(w)
+        off = np.concatenate([[0], np.cumsum(lens[w])[:-1]])
+        for v in range(m):
+            if not returns[w, v] >= NEAR_BOTTLENECK * z[w]:
+                continue
+            seg = ops[w, off[v]:off[v] + lens[w, v]]
+            for i in np.flatnonzero(seg & 1):
+                ent.append((w, v, int(i), int(off[v] + i), 0))
+    return ent, alive
+
+
+def cross_entries(ops, lens, z, returns, active):
+    m = lens.shape[1]
+    ent, cnt = [], []
+    for w in active:
+        b = int(np.argmax(returns[w]))  # Schedule.bottleneck: first max
+        off = np.concatenate([[0], np.cumsum(lens[w])[:-1]])
+        total = int(lens[w].sum())
+        flat = ops[w, :total]
+        cust = (flat >> 1) + 1
+        route = np.repeat(np.arange(m), lens[w])
+        for c in sorted(set(cust[off[b]:off[b] + lens[w, b]].tolist())):
+            pos = np.flatnonzero(cust == c)
+            f1, f2 = int(pos[0]), int(pos[1])
+            for u in range(m):
+                if u == b:
+                    continue
+                L = int(lens[w, u]) - int((route[pos] == u).sum())
+                ent.append((w, c, u, f1, f2))
+                cnt.append((L + 1) * (L + 2) // 2)
+    return ent, np.asarray(cnt, np.int64)

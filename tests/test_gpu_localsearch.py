@@ -116,3 +116,34 @@ def test_ls_topk_kernel_vs_numpy():
         assert tn[w] == order.size, w
         np.testing.assert_array_equal(ti[w, :tn[w]], order)
         np.testing.assert_array_equal(tz[w, :tn[w]], z[order])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key,count", [("gr17", 12), ("eil51", 9), ("a280", 5), ("dsj1000", 4)])
+def test_ls_entries_kernel_vs_host(key, count):
+    """vrp_ls_entries (both kinds) equals the host entry builders: same
+    entries in the same order, same candidate starts, on a subset of active
+    solutions, with one vehicle's return set exactly to 0.9 z (kept: >=)."""
+    inst = config_instance(key)
+    dec = O.decode_batch(inst, I.chromosomes(inst.n, count, (84, CID.get(key, 9))))
+    ops, lens = dec["ops"].astype(np.int32), dec["lens"].astype(np.int32)
+    ops_t, lens_t = torch.from_numpy(ops).cuda(), torch.from_numpy(lens).cuda()
+    z, returns = LS._evaluate(inst, ops_t, lens_t)
+    returns = returns.copy()
+    v = int(np.argmin(returns[0]))
+    returns[0, v] = 0.9 * z[0]
+    active = [w for w in range(count) if w % 3 != 1]
+    for kind in (0, 1):
+        ent_t, start_t, ccount, coff = LS.entries(inst, kind, ops_t, lens_t, z, returns, active)
+        if kind == 0:
+            ent, _ = H.pickup_entries(ops, lens, z, returns, active)
+            cnt = np.full(len(ent), 2 * inst.n + inst.m - 2, np.int64)
+        else:
+            ent, cnt = H.cross_entries(ops, lens, z, returns, active)
+        ent = np.asarray(ent, np.int32).reshape(-1, 5)
+        starts = np.concatenate([[0], np.cumsum(cnt)[:-1]]).astype(np.int64)
+        np.testing.assert_array_equal(ent_t.cpu().numpy(), ent, err_msg=f"kind {kind}")
+        np.testing.assert_array_equal(start_t.cpu().numpy(), starts, err_msg=f"kind {kind}")
+        per = np.zeros(count, np.int64)
+        np.add.at(per, ent[:, 0], cnt)
+        np.testing.assert_array_equal(ccount, per)
