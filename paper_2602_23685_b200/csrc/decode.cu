@@ -148,11 +148,18 @@ sort_kernel(const double *__restrict__ genes, int64_t gstride, int64_t N, int tw
 // network's O(n log^2 n).  A chromosome with a bucket of more than MAXB
 // entries (many equal or clustered priorities) is flagged for sort_kernel.
 constexpr int MAXB = 48;
+constexpr int SU = 8;  // priorities loaded per lane per batch
 
 // bucket count: a power of two near n (about two priorities per bucket), 64..1024
+#ifndef VRP_BUCKET_PER
+#define VRP_BUCKET_PER 2  // priorities per bucket (target)
+#endif
+#ifndef VRP_BUCKET_MAX
+#define VRP_BUCKET_MAX 1024
+#endif
 __host__ __device__ inline int bucket_count(int two_n) {
-    const int b = pow2_at_least(two_n / 2);
-    return b < 64 ? 64 : (b > 1024 ? 1024 : b);
+    const int b = pow2_at_least(two_n / VRP_BUCKET_PER);
+    return b < 64 ? 64 : (b > VRP_BUCKET_MAX ? VRP_BUCKET_MAX : b);
 }
 
 __device__ __forceinline__ int bucket_of(double x, int nb) {
@@ -161,8 +168,11 @@ __device__ __forceinline__ int bucket_of(double x, int nb) {
     return 1 + (int)(x * (double)(nb - 2));
 }
 
+// per warp: bucket counters, the scattered indices and their keys' upper 32
+// bits (the insertion sort compares those in shared memory and reads the full
+// keys only on a tie of the upper halves)
 __host__ __device__ inline size_t bucket_sort_bytes(int n) {
-    return align16(4 * (size_t)bucket_count(2 * n)) + align16(2 * (size_t)(2 * n));
+    return align16(4 * (size_t)bucket_count(2 * n)) + align16(2 * (size_t)(2 * n)) + align16(4 * (size_t)(2 * n));
 }
 
 __global__ void __launch_bounds__(256)
@@ -171,28 +181,42 @@ bucket_sort_kernel(const double *__restrict__ genes, int64_t gstride, int64_t N,
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     unsigned char *base = smem + (size_t)warp * bucket_sort_bytes(two_n / 2);
-    const int NB = bucket_count(two_n), PER = NB / 32;
+    const int NB = bucket_count(two_n);
     int *cnt = reinterpret_cast<int *>(base);
     uint16_t *out = reinterpret_cast<uint16_t *>(base + align16(4 * (size_t)NB));
-    const unsigned lt = lanemask_lt();
+    uint32_t *khi = reinterpret_cast<uint32_t *>(base + align16(4 * (size_t)NB) + align16(2 * (size_t)two_n));
     for (int64_t chrom = (int64_t)blockIdx.x * wpb + warp; chrom < N; chrom += (int64_t)gridDim.x * wpb) {
         const double *g = genes + chrom * gstride;
         for (int b = lane; b < NB; b += 32) cnt[b] = 0;
         __syncwarp();
-        for (int i = lane; i < two_n; i += 32) atomicAdd(&cnt[bucket_of(__ldg(g + i), NB)], 1);
-        __syncwarp();
-        // exclusive prefix (lane owns NB/32 consecutive buckets) + largest bucket
-        int run = 0, big = 0;
-        for (int j = 0; j < PER; ++j) {
-            const int c = cnt[lane * PER + j];
-            run += c;
-            big = c > big ? c : big;
-        }
-        int incl = run;
+        // the priorities are read in batches of SU per lane, so SU loads are in
+        // flight instead of one per shared-memory atomic
+        for (int i0 = 0; i0 < two_n; i0 += 32 * SU) {
+            double x[SU];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(VRP_FULL_MASK, incl, o);
-            if (lane >= o) incl += y;
+            for (int u = 0; u < SU; ++u) {
+                const int i = i0 + u * 32 + lane;
+                x[u] = i < two_n ? __ldg(g + i) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < SU; ++u)
+                if (i0 + u * 32 + lane < two_n) atomicAdd(&cnt[bucket_of(x[u], NB)], 1);
+        }
+        __syncwarp();
+        // exclusive prefix over the buckets, 32 consecutive buckets per step
+        // (lane = bucket: conflict-free), and the largest bucket
+        int carry = 0, big = 0;
+        for (int j = 0; j < NB; j += 32) {
+            const int c = cnt[j + lane];
+            big = c > big ? c : big;
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(VRP_FULL_MASK, incl, o);
+                if (lane >= o) incl += y;
+            }
+            cnt[j + lane] = carry + incl - c;  // bucket start, advanced by the scatter
+            carry += __shfl_sync(VRP_FULL_MASK, incl, 31);
         }
         for (int o = 16; o; o >>= 1) {
             const int y = __shfl_xor_sync(VRP_FULL_MASK, big, o);
@@ -203,33 +227,48 @@ bucket_sort_kernel(const double *__restrict__ genes, int64_t gstride, int64_t N,
             __syncwarp();
             continue;
         }
-        int at = incl - run;
-        for (int j = 0; j < PER; ++j) {
-            const int c = cnt[lane * PER + j];
-            cnt[lane * PER + j] = at;  // bucket start, advanced by the scatter
-            at += c;
+        __syncwarp();
+        for (int i0 = 0; i0 < two_n; i0 += 32 * SU) {
+            double x[SU];
+#pragma unroll
+            for (int u = 0; u < SU; ++u) {
+                const int i = i0 + u * 32 + lane;
+                x[u] = i < two_n ? __ldg(g + i) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < SU; ++u) {
+                const int i = i0 + u * 32 + lane;
+                if (i < two_n) {
+                    const int pos = atomicAdd(&cnt[bucket_of(x[u], NB)], 1);
+                    out[pos] = (uint16_t)i;
+                    khi[pos] = (uint32_t)(order_key(x[u]) >> 32);
+                }
+            }
         }
         __syncwarp();
-        for (int i = lane; i < two_n; i += 32) {
-            const int pos = atomicAdd(&cnt[bucket_of(__ldg(g + i), NB)], 1);
-            out[pos] = (uint16_t)i;
-        }
-        __syncwarp();
-        // cnt[b] is now bucket b's end; sort each bucket by (key, index)
+        // cnt[b] is now bucket b's end; sort each bucket by (key, index) --
+        // upper key halves from shared memory, full keys only on a tie of those
         for (int b = lane; b < NB; b += 32) {
             const int e = cnt[b], s0 = b ? cnt[b - 1] : 0;
             for (int i = s0 + 1; i < e; ++i) {
                 const uint16_t xi = out[i];
-                const uint64_t kx = order_key(__ldg(g + xi));
+                const uint32_t hx = khi[i];
                 int j = i - 1;
                 while (j >= s0) {
                     const uint16_t yj = out[j];
-                    const uint64_t ky = order_key(__ldg(g + yj));
-                    if (ky < kx || (ky == kx && yj < xi)) break;
+                    const uint32_t hy = khi[j];
+                    bool before = hy < hx;  // y sorts before x: stop
+                    if (hy == hx) {
+                        const uint64_t kx = order_key(__ldg(g + xi)), ky = order_key(__ldg(g + yj));
+                        before = ky < kx || (ky == kx && yj < xi);
+                    }
+                    if (before) break;
                     out[j + 1] = yj;
+                    khi[j + 1] = hy;
                     --j;
                 }
                 out[j + 1] = xi;
+                khi[j + 1] = hx;
             }
         }
         __syncwarp();
@@ -238,7 +277,6 @@ bucket_sort_kernel(const double *__restrict__ genes, int64_t gstride, int64_t N,
         if (lane == 0) fallback[chrom] = 0;
         __syncwarp();
     }
-    (void)lt;
 }
 
 // MC > 0 fixes the fleet size at compile time (MC == I.m): the argmin
