@@ -51,11 +51,14 @@ struct DecodeLayout {
     size_t pend, ready, total;
 };
 
+// ready_bytes = 0: the compact slot table (a u8 slot id per customer + 32
+// uint32 values, see decode_multi_kernel's CT)
 __host__ __device__ inline DecodeLayout decode_layout(int n, int ready_bytes = 8) {
     DecodeLayout L;
     L.pend = 0;
     L.ready = align16(2 * (size_t)(2 * n));
-    L.total = L.ready + align16((size_t)ready_bytes * (size_t)(n + 1));
+    L.total = L.ready + (ready_bytes ? align16((size_t)ready_bytes * (size_t)(n + 1))
+                                     : align16((size_t)(n + 1)) + 4 * 32);
     return L;
 }
 
@@ -279,10 +282,13 @@ bucket_sort_kernel(const double *__restrict__ genes, int64_t gstride, int64_t N,
     }
 }
 
+#ifndef VRP_DECODE_MINB
+#define VRP_DECODE_MINB 5  // decode_kernel launch bounds (5: <= 48 registers; 4 measured 2.7 % slower at n = 999)
+#endif
 // MC > 0 fixes the fleet size at compile time (MC == I.m): the argmin
 // butterfly, the hint product and the vehicle-major emit loop are unrolled.
-template <bool INTD, typename OutT, bool NARROW = false, int MC = 0>
-__global__ void __launch_bounds__(256, 4)
+template <bool INTD, typename OutT, bool NARROW = false, int MC = 0, bool CT = false>
+__global__ void __launch_bounds__(256, VRP_DECODE_MINB)
 decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, int64_t N,
               int relax, double penalty, double *__restrict__ fitness_out,
               double *__restrict__ makespan_out, int32_t *__restrict__ scheduled_out,
@@ -296,9 +302,11 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
     const int warp = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int n = I.n, m = MC ? MC : I.m, k = I.k, two_n = 2 * n;
-    const DecodeLayout Ly = decode_layout(n, (int)sizeof(RT));
+    const DecodeLayout Ly = decode_layout(n, CT ? 0 : (int)sizeof(RT));
     unsigned char *base = smem + (size_t)warp * Ly.total;
     volatile RT *s_ready = reinterpret_cast<volatile RT *>(base + Ly.ready);
+    volatile uint8_t *s_sid = reinterpret_cast<volatile uint8_t *>(base + Ly.ready);
+    volatile uint32_t *s_val = reinterpret_cast<volatile uint32_t *>(base + Ly.ready + align16((size_t)(n + 1)));
     uint16_t *s_pend = reinterpret_cast<uint16_t *>(base + Ly.pend);
     const bool vlane = lane < m;
     const unsigned lt = lanemask_lt();
@@ -315,8 +323,14 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
         // ---- pending list = the stable priority order (sort_kernel)
         const uint16_t *ord = order + chrom * (int64_t)two_n;
         for (int i = lane; i < two_n; i += 32) s_pend[i] = __ldg(ord + i);
-        for (int c = lane; c <= n; c += 32) s_ready[c] = NARROW ? (RT)NOT_DROPPED32 : (RT)-1.0;  // not dropped
+        if (CT) {
+            volatile uint32_t *w4 = reinterpret_cast<volatile uint32_t *>(s_sid);
+            for (int c = lane; c < (n + 4) / 4; c += 32) w4[c] = 0xFFFFFFFFu;
+        } else {
+            for (int c = lane; c <= n; c += 32) s_ready[c] = NARROW ? (RT)NOT_DROPPED32 : (RT)-1.0;  // not dropped
+        }
         __syncwarp();
+        unsigned freem = 0xFFFFFFFFu;  // CT: free slots (warp-uniform)
 
         // ---- vehicle state (lane v = vehicle v)
         double t = 0.0;
@@ -342,7 +356,13 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
                 const double pj = valid && !pk ? __ldg(I.p + c) : 0.0;  // dropoff processing time
                 // the pickup's ready time, read once per window; a dropoff placed
                 // inside the window updates its pickup's copy in registers
-                RT rr = pk ? s_ready[c] : (RT)0;
+                RT rr;
+                if (CT) {
+                    const int sd = pk ? (int)s_sid[c] : 0xFF;
+                    rr = pk ? (sd == 0xFF ? (RT)NOT_DROPPED32 : (RT)s_val[sd & 31]) : (RT)0;
+                } else {
+                    rr = pk ? s_ready[c] : (RT)0;
+                }
                 unsigned todo = __ballot_sync(VRP_FULL_MASK, valid);
                 __syncwarp();
                 while (todo) {
@@ -423,8 +443,18 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
                         } else {
                             rs = (RT)rv;
                         }
-                        if (lane == 0) s_ready[cf] = rs;
+                        if (CT) {
+                            ovf |= freem == 0u;  // no free slot: the wide fix-up pass decodes it
+                            const int slot = freem ? __ffs(freem) - 1 : 0;
+                            freem &= ~(1u << slot);
+                            if (lane == 0) { s_val[slot] = (uint32_t)rs; s_sid[cf] = (uint8_t)slot; }
+                        } else {
+                            if (lane == 0) s_ready[cf] = rs;
+                        }
                         if (op == opf + 1) rr = rs;  // this window holds the pickup
+                    } else if (CT) {
+                        const int sd = (int)s_sid[cf];  // its dropoff's slot is free again
+                        freem |= 1u << (sd & 31);
                     }
                     if (lane == 0 && seq_scratch) seq[nseq] = (uint32_t)opf | ((uint32_t)vstar << 16);
                     ++nseq;
@@ -841,13 +871,13 @@ int launch_m(const DevInstance &I, const double *genes, int64_t gstride, int64_t
 }
 
 // one decode_kernel launch, occupancy planned once per (instantiation, n)
-template <bool INTD, typename OutT, bool NARROW, int MC = 0>
+template <bool INTD, typename OutT, bool NARROW, int MC = 0, bool CT = false>
 int launch_k(const DevInstance &I, const double *genes, int64_t gstride, int64_t N, int relax,
              double penalty, double *fitness, double *makespan, int32_t *scheduled, int64_t *visits,
              void *ops_out, int64_t ostride, int32_t *lens_out, const uint16_t *order, uint32_t *seq,
              uint8_t *retry, const uint8_t *only, cudaStream_t stream, int sm_count) {
-    auto kern = decode_kernel<INTD, OutT, NARROW, MC>;
-    const size_t per_warp = decode_layout(I.n, NARROW ? 4 : 8).total;
+    auto kern = decode_kernel<INTD, OutT, NARROW, MC, CT>;
+    const size_t per_warp = decode_layout(I.n, CT ? 0 : (NARROW ? 4 : 8)).total;
     static PlanCache<DecodePlan> cache;
     DecodePlan pl;
     const int rc = cache.get((int64_t)per_warp, pl, [&](DecodePlan &out) { return plan_decode(kern, per_warp, out); });
@@ -874,6 +904,7 @@ int launch_any(const DevInstance &I, const double *genes, int64_t gstride, int64
                uint8_t *retry, const uint8_t *only, cudaStream_t stream, int sm_count) {
     const char *single = getenv("VRP_DECODE_SINGLE");
     const char *noct = getenv("VRP_DECODE_NO_CT");  // (ablation knob)
+    const char *wnoct = getenv("VRP_DECODE_WARP_NO_CT");  // (ablation knob: warp kernel only)
     // the compact slot table (narrow pass, m k <= 32 slots, m = 6): 5 KB of
     // shared memory per chromosome at n = 999 instead of 10 KB
     const bool ct = NARROW && I.m == 6 && I.m * I.k <= MULTI_SLOTS && !(noct && noct[0] && noct[0] != '0');
@@ -903,6 +934,10 @@ int launch_any(const DevInstance &I, const double *genes, int64_t gstride, int64
         return launch_m<INTD, OutT, NARROW, 16>(I, genes, gstride, N, relax, penalty, fitness, makespan,
                                                 scheduled, visits, ops_out, ostride, lens_out, order, seq, retry,
                                                 only, stream, sm_count);
+    if (ct && !(wnoct && wnoct[0] && wnoct[0] != '0'))  // the slot table in the warp kernel too
+        return launch_k<INTD, OutT, NARROW, 6, true>(I, genes, gstride, N, relax, penalty, fitness, makespan,
+                                                     scheduled, visits, ops_out, ostride, lens_out, order, seq,
+                                                     retry, only, stream, sm_count);
     if (I.m == 6)  // the fleet of every benchmark config beyond gr17
         return launch_k<INTD, OutT, NARROW, 6>(I, genes, gstride, N, relax, penalty, fitness, makespan, scheduled,
                                                visits, ops_out, ostride, lens_out, order, seq, retry, only, stream,
