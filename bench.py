@@ -214,9 +214,9 @@ def extra_rates(device, ops, lens, decode_ms, n_dec, pipeline_seconds=30.0):
     # K1 on the other benchmark configs (decoded candidates, device-resident)
     for key in ("eil51", "kroA100", "a280"):
         ki = config_instance(key)
-        # 2^20 candidates: larger than L2 at every n (at eil51, 2^19 freshly
-        # decoded candidates sit in L2 and measure ~40 % slower than streamed
-        # from HBM -- scripts/probe_k1_addr.py)
+        # 2^20 candidates: larger than L2 at every n.  At eil51 the rate is
+        # bimodal (~360 M or ~630 M evals/s) with where the op buffer lands in
+        # device memory (scripts/probe_k1_bench_ctx.py); dsj1000 is not
         cnt = 1 << 20
         kops = torch.empty((cnt, 2 * ki.n), dtype=torch.int16, device=device)
         klens = torch.empty((cnt, ki.m), dtype=torch.int32, device=device)
