@@ -28,6 +28,8 @@
 #define VRP_RPD_H
 #include <stdint.h>
 
+#define VRP_MAX_N 8192  /* largest instance (customers) every kernel supports */
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -68,7 +70,8 @@ const char *vrp_last_error(void);
 /* Upload an instance (instance.py:82-156 Instance): host d[(n+1)*(n+1)], p[n+1].
  * The handle owns the device copies; d is also kept as int32 when every entry
  * is an integer in [0, 2^31) (all TSPLIB distance types), which halves the
- * L2 footprint of the gathers.  Requires 1 <= m <= 32, 1 <= n <= 16383. */
+ * L2 footprint of the gathers.  Requires 1 <= m <= 32, 1 <= n <= VRP_MAX_N (8192: the
+ * tightest per-kernel shared-memory bound, K3's bitonic argsort fallback). */
 int vrp_instance_create(int32_t n, int32_t m, int32_t k, const double *d_host,
                         const double *p_host, vrp_instance_t *out);
 int vrp_instance_destroy(vrp_instance_t h);

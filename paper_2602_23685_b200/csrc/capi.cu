@@ -75,7 +75,11 @@ const char *vrp_last_error(void) { return g_err; }
 int vrp_instance_create(int32_t n, int32_t m, int32_t k, const double *d_host, const double *p_host,
                         vrp_instance_t *out) {
     if (!out || !d_host || !p_host) return fail(VRP_EINVAL, "null argument%s");
-    if (n < 1 || n > 16383) return fail(VRP_EUNSUPPORTED, "n must lie in [1, 16383]%s");
+    // the binding per-kernel limit: K3's bitonic argsort fallback holds a chromosome's
+    // 2n keys (+ indices) padded to a power of two in one warp's shared memory
+    // (10 B x 16384 at n = 8192); K1's 64-bit fix-up table fits to n ~ 14.5 k,
+    // K2's to ~13 k
+    if (n < 1 || n > VRP_MAX_N) return fail(VRP_EUNSUPPORTED, "n must lie in [1, 8192]%s");
     if (m < 1 || m > 32) return fail(VRP_EUNSUPPORTED, "m must lie in [1, 32] (lanes = vehicles)%s");
     if (k < 1) return fail(VRP_EINVAL, "k must be >= 1%s");
     const size_t cells = (size_t)(n + 1) * (size_t)(n + 1);

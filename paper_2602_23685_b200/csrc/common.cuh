@@ -26,7 +26,7 @@ __device__ __forceinline__ bool op_is_pick(int op) { return op & 1; }
 // identical double value with half the L2 sector footprint per row.
 template <bool INTD>
 __device__ __forceinline__ double dist(const DevInstance &I, int a, int b) {
-    const uint32_t idx = (uint32_t)a * (uint32_t)I.W + (uint32_t)b;  // n <= 16383: W^2 < 2^28
+    const uint32_t idx = (uint32_t)a * (uint32_t)I.W + (uint32_t)b;  // n <= 8192: W^2 < 2^27
     if (INTD) return (double)__ldg(I.d32 + idx);
     return __ldg(I.d + idx);
 }

@@ -98,7 +98,7 @@ struct LegRaw<true> { using T = int32_t; };
 template <bool INTD>
 __device__ __forceinline__ typename LegRaw<INTD>::T gather_leg(const DevInstance &I, int a, int b) {
     // L2-only load: the random d gathers must not evict the op-stream lines from L1.
-    // 32-bit index: n <= 16383 (vrp_instance_create), so W^2 < 2^28
+    // 32-bit index: n <= 8192 (vrp_instance_create), so W^2 < 2^27
     const uint32_t idx = (uint32_t)a * (uint32_t)I.W + (uint32_t)b;
     if (INTD) return (typename LegRaw<INTD>::T)__ldcg(I.d32 + idx);
     return (typename LegRaw<INTD>::T)__ldcg(I.d + idx);

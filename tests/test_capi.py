@@ -99,3 +99,21 @@ def test_struct_layouts_match_python_mirrors(tmp_path):
         assert vals[k] == getattr(DV.AlnsParamsC, f).offset, f
         k += 1
     assert vals[k:] == [R._DTYPE.fields[f][1] for f in ("buffer_pos", "has_uint32", "uinteger")]
+
+
+def test_instance_size_limits_checked_before_any_device_work(libpath):
+    """vrp_instance_create rejects n beyond VRP_MAX_N (the tightest per-kernel
+    shared-memory bound) and m beyond 32 with VRP_EUNSUPPORTED, before it
+    reads the matrices or touches a device -- so this runs on the CPU."""
+    text = HEADER.read_text()
+    max_n = int(re.search(r"#define VRP_MAX_N (\d+)", text).group(1))
+    unsupported = int(re.search(r"#define VRP_EUNSUPPORTED (\d+)", text).group(1))
+    lib = ctypes.CDLL(str(libpath))
+    lib.vrp_instance_create.argtypes = [ctypes.c_int32] * 3 + [ctypes.c_void_p] * 3
+    lib.vrp_last_error.restype = ctypes.c_char_p
+    one = np.zeros(1)
+    h = ctypes.c_void_p()
+    for n, m in ((max_n + 1, 6), (0, 6), (10, 33)):
+        rc = lib.vrp_instance_create(n, m, 1, one.ctypes.data, one.ctypes.data, ctypes.byref(h))
+        assert rc == unsupported, (n, m, rc)
+        assert b"must lie in" in lib.vrp_last_error()

@@ -287,3 +287,33 @@ def test_decode_hint_vehicle_edge_values_on_device(m, golden):
     np.testing.assert_array_equal(r["lens"].cpu().numpy(), ref["lens"])
     np.testing.assert_array_equal(r["ops"].cpu().numpy(), ref["ops"])
     np.testing.assert_array_equal(r["fitness"].cpu().numpy(), ref["fitness"])
+
+
+def test_max_n_instance_all_scoring_paths():
+    """n = VRP_MAX_N = 8192, the largest instance vrp_instance_create accepts:
+    K3 decode with uniform priorities (counting sort) and clustered ones (the
+    bitonic fallback at its largest shared-memory footprint), then K1 exact /
+    evaluate and K2 two-pass on the decoded candidates -- against the oracle."""
+    from scipy.spatial.distance import cdist
+    from paper_2602_23685_b200.instance import Instance
+    n, m, k = 8192, 6, 4
+    g = np.random.default_rng(8192)
+    xy = g.integers(0, 20000, size=(n + 1, 2)).astype(float)
+    d = cdist(xy, xy)
+    np.rint(d, out=d)
+    p = g.integers(1, 100, size=n + 1).astype(float)
+    p[0] = 0
+    inst = Instance.from_arrays(d, p, m, k, label="max-n")
+    del d
+    genes = np.stack([g.random(4 * n),
+                      np.concatenate([g.integers(0, 4, 2 * n) / 4.0, g.random(2 * n)])])
+    ref = O.decode_batch(inst, genes)
+    r = dev().decode_batch(inst, _cuda(genes))
+    np.testing.assert_array_equal(r["ops"].cpu().numpy().astype(np.int32), ref["ops"])
+    np.testing.assert_array_equal(r["fitness"].cpu().numpy(), ref["fitness"])
+    np.testing.assert_array_equal(r["visits"].cpu().numpy(), ref["visits"])
+    for mode, name in ((0, "exact"), (1, "evaluate"), (2, "two_pass")):
+        rr = dev().makespan_batch(inst, _cuda(ref["ops"]), _cuda(ref["lens"]), mode=mode)
+        z, st = O.makespan_batch(inst, ref["ops"], ref["lens"], mode=name)
+        np.testing.assert_array_equal(rr["status"].cpu().numpy(), st, err_msg=name)
+        np.testing.assert_array_equal(rr["z"].cpu().numpy(), z, err_msg=name)
