@@ -261,11 +261,25 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 if (cg >= N || mg) continue;
                 uint32_t *bt = reinterpret_cast<uint32_t *>(wbase + (size_t)gg * CL.total + CL.bits);
                 bool dup = false;
-                for (int j = lane; j < tg; j += 32) {
-                    const int op = (int)__ldg(ops + cg * stride + j);
-                    if (op < 0 || op >= two_n) { dup = true; continue; }
-                    const uint32_t bit = 1u << (op & 31);
-                    dup |= (atomicOr(&bt[op >> 5], bit) & bit) != 0;
+                // VB op codes in flight per lane (the first touch of the row
+                // comes from HBM; one load per shared atomic left the warp
+                // waiting on every load)
+                constexpr int VB = 8;
+                for (int j0 = 0; j0 < tg; j0 += 32 * VB) {
+                    int ov[VB];
+#pragma unroll
+                    for (int u = 0; u < VB; ++u) {
+                        const int j = j0 + u * 32 + lane;
+                        ov[u] = j < tg ? (int)__ldg(ops + cg * stride + j) : 0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < VB; ++u) {
+                        if (j0 + u * 32 + lane >= tg) continue;
+                        const int op = ov[u];
+                        if (op < 0 || op >= two_n) { dup = true; continue; }
+                        const uint32_t bit = 1u << (op & 31);
+                        dup |= (atomicOr(&bt[op >> 5], bit) & bit) != 0;
+                    }
                 }
                 const bool anyd = __any_sync(VRP_FULL_MASK, dup);
                 if (glane && g == gg) mal |= anyd;
