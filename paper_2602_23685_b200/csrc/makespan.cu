@@ -41,6 +41,12 @@ constexpr int ST_RETRY = 4;                 // internal: narrow ready table over
 constexpr uint32_t NOT_READY32 = 0xFFFFFFFFu;
 constexpr int OPS_AHEAD = 8;   // op codes in registers (positions i .. i+7)
 constexpr int LEGS_AHEAD = 4;  // gathered legs in registers (positions i .. i+3)
+#ifndef K2_LEGS_AHEAD
+#define K2_LEGS_AHEAD 8  // two-pass (K2) pipeline depths: shared memory caps K2 at 8 warps/SM (4 / 8: 1.78 s, 8 / 12: 1.70 s LS cross pass at n = 999)
+#endif
+#ifndef K2_OPS_AHEAD
+#define K2_OPS_AHEAD 12
+#endif
 #ifndef VRP_K1_RA
 #define VRP_K1_RA 0  // run-ahead ops per lockstep round (exact mode, slot table); measured slower, see DESIGN.md
 #endif
@@ -288,7 +294,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         mal = (__ballot_sync(VRP_FULL_MASK, live && mal) & gmask) != 0;
         const bool run = live && !mal;
 
-        RouteStream<OpT, INTD> rs;
+        RouteStream<OpT, INTD, MODE == MODE_TWO ? K2_OPS_AHEAD : OPS_AHEAD, MODE == MODE_TWO ? K2_LEGS_AHEAD : LEGS_AHEAD> rs;
         rs.init(I, row + (run && L > 0 ? off : 0), run ? L : 0, two_n);
         TT t = 0;
         int s = 0, lo = 0, hi = k, lastc = 0;
