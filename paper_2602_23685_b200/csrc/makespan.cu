@@ -384,7 +384,6 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                     const bool own = dgo && mine;
                     if (own) slot = __ffs(mine) - 1;
                     const bool need = dgo && !mine;
-                    bool stuck = false;
                     if (__any_sync(VRP_FULL_MASK, need)) {
                         // borrow from the next route's class: its lowest free slot, or
                         // the second lowest when that route takes its own lowest now
@@ -392,16 +391,16 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                         const unsigned nx = freem & cls_next;
                         const unsigned cand = nxt_own ? (nx & (nx - 1)) : nx;
                         if (need && cand) slot = __ffs(cand) - 1;
-                        stuck = need && !cand;
-                    }
-                    if (__any_sync(VRP_FULL_MASK, stuck)) {
-                        const unsigned dm = __ballot_sync(VRP_FULL_MASK, dgo) & gmask;
-                        unsigned x = freem;
-                        const int below = __popc(dm & lanemask_lt());
-                        slot = SLOTS;
-                        for (int q = 0, kq = __popc(dm); q < kq && x; ++q) {
-                            if (q == below && dgo) slot = __ffs(x) - 1;
-                            x &= x - 1;
+                        const bool stuck = need && !cand;
+                        if (__any_sync(VRP_FULL_MASK, stuck)) {  // (only ever after a borrow)
+                            const unsigned dm = __ballot_sync(VRP_FULL_MASK, dgo) & gmask;
+                            unsigned x = freem;
+                            const int below = __popc(dm & lanemask_lt());
+                            slot = SLOTS;
+                            for (int q = 0, kq = __popc(dm); q < kq && x; ++q) {
+                                if (q == below && dgo) slot = __ffs(x) - 1;
+                                x &= x - 1;
+                            }
                         }
                     }
                     // slots taken (were free) and returned by pickups (were taken)
