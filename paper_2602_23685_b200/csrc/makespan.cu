@@ -84,6 +84,13 @@ __host__ __device__ inline CandLayout cand_layout(int n, int mode, int ready_byt
 
 __host__ __device__ inline size_t block_p_bytes(int n) { return align16(sizeof(double) * (size_t)(n + 1)); }
 
+// a << b with PTX semantics: b >= 32 gives 0 (C++ leaves it undefined)
+__device__ __forceinline__ unsigned shl_clamped(unsigned a, unsigned b) {
+    unsigned r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
 __device__ __forceinline__ void cap_step(int op, int k, int &s, int &lo, int &hi) {
     if (op & 1) { int room = k - 1 - s; hi = room < hi ? room : hi; ++s; }
     else        { int need = 1 - s;     lo = need > lo ? need : lo; --s; }
@@ -405,8 +412,10 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                     }
                     // slots taken (were free) and returned by pickups (were taken)
                     // flip; the XOR of all of them is one OR over the candidate's lanes
-                    unsigned tg = (dgo && slot < SLOTS) ? (1u << slot) : 0u;
-                    if (go && pick && sid < SLOTS) tg |= 1u << sid;
+                    // (PTX shl clamps shift amounts >= 32 to a zero result: slot = SLOTS
+                    // means none taken, sid = 0xFF none returned)
+                    unsigned tg = shl_clamped(1u, dgo ? (unsigned)slot : 32u) |
+                                  shl_clamped(1u, (go && pick) ? (unsigned)sid : 32u);
                     tg |= __shfl_sync(VRP_FULL_MASK, tg, pt1);
                     if (m > 2) tg |= __shfl_sync(VRP_FULL_MASK, tg, pt2);
                     if (m > 4) tg |= __shfl_sync(VRP_FULL_MASK, tg, pt4);
