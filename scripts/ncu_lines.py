@@ -1,6 +1,9 @@
 """Attribute an ncu --set full capture's per-instruction counts and stall
 samples to source lines (nvdisasm -g line table of the in-tree library).
-    python scripts/ncu_lines.py REPORT.ncu-rep KERNEL_SUBSTRING CUBIN_STEM [top]"""
+    python scripts/ncu_lines.py REPORT.ncu-rep KERNEL_SUBSTRING CUBIN_STEM [top]
+KERNEL_SUBSTRING must pick the profiled instantiation out of the cubin (a
+piece of its mangled name, e.g. makespan_kernelIsLb1ELi0ELb0ELb1ELb1ELi6ELi0E):
+another instantiation of the same template has another address map."""
 import collections
 import csv
 import io
