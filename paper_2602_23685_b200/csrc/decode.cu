@@ -103,15 +103,28 @@ __device__ __forceinline__ void bitonic_sort(uint64_t *key, uint16_t *idx, int P
 
 // warp-uniform: can any vehicle take a dropoff / a pickup now, and (strict
 // mode) the latest clock among vehicles that can take a pickup
+// mhalf: the max runs over lanes [0, 2 mhalf) (which hold the m vehicles) and
+// is broadcast from lane 0 -- 3 butterfly levels instead of 5 at m = 6
 __device__ __forceinline__ void fleet_flags(bool vlane, double t, int net, int lo, int hi, int k,
                                             int relax, bool &any_drop, bool &any_pick,
-                                            double &pick_maxT) {
+                                            double &pick_maxT, int mhalf = 16) {
     int need = 1 - net, room = k - 1 - net;
     bool cd = vlane && ((need > lo ? need : lo) <= hi);
     bool cp = vlane && (lo <= (room < hi ? room : hi));
     any_drop = __any_sync(VRP_FULL_MASK, cd);
     any_pick = __any_sync(VRP_FULL_MASK, cp);
-    pick_maxT = relax ? 0.0 : warp_max(cp ? t : -DBL_MAX);
+    if (relax) {
+        pick_maxT = 0.0;
+    } else if (mhalf >= 16) {
+        pick_maxT = warp_max(cp ? t : -DBL_MAX);
+    } else {
+        double x = cp ? t : -DBL_MAX;
+        for (int o = mhalf; o; o >>= 1) {
+            const double y = __shfl_xor_sync(VRP_FULL_MASK, x, o);
+            x = y > x ? y : x;
+        }
+        pick_maxT = __shfl_sync(VRP_FULL_MASK, x, 0);
+    }
 }
 
 // Stable argsort of every chromosome's 2n priorities (brkga.py:116), one warp
@@ -337,7 +350,7 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
         int loc = 0, net = 0, lo = 0, hi = k, cnt = 0;
         bool any_drop, any_pick;
         double pick_maxT;
-        fleet_flags(vlane, t, net, lo, hi, k, relax, any_drop, any_pick, pick_maxT);
+        fleet_flags(vlane, t, net, lo, hi, k, relax, any_drop, any_pick, pick_maxT, mhalf);
 
         int npend = two_n, nseq = 0;
         int64_t visits = 0;
@@ -459,7 +472,7 @@ decode_kernel(DevInstance I, const double *__restrict__ genes, int64_t gstride, 
                     if (lane == 0 && seq_scratch) seq[nseq] = (uint32_t)opf | ((uint32_t)vstar << 16);
                     ++nseq;
                     progressed = true;
-                    fleet_flags(vlane, t, net, lo, hi, k, relax, any_drop, any_pick, pick_maxT);
+                    fleet_flags(vlane, t, net, lo, hi, k, relax, any_drop, any_pick, pick_maxT, mhalf);
                     __syncwarp();
                 }
                 __syncwarp();
