@@ -264,9 +264,9 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
             }
         }
         __syncwarp();
-        if (MODE != MODE_EXACT) {
+        if (MODE == MODE_EVAL) {
             // duplicates / range (schedule.py:134-156): the whole warp streams
-            // each candidate's ops, coalesced
+            // each candidate's ops, coalesced (two-pass: inside pass 1, below)
             for (int gg = 0; gg < G; ++gg) {
                 const int64_t cg = base + gg;
                 const int tg = __shfl_sync(VRP_FULL_MASK, total, gg * m);
@@ -305,13 +305,21 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
         rs.init(I, row + (run && L > 0 ? off : 0), run ? L : 0, two_n);
         TT t = 0;
         int s = 0, lo = 0, hi = k, lastc = 0;
-        bool dead = false, bad_ops = false, ovf = false;
+        bool dead = false, bad_ops = false, ovf = false, dup = false;
 
         if (MODE == MODE_TWO) {
-            // pass 1: no-wait walk; ready = dropoff time + p (schedule.py:371-378)
+            // pass 1: no-wait walk; ready = dropoff time + p (schedule.py:371-378).
+            // Each lane also marks its route's ops in the candidate's bitmap:
+            // a second mark is a duplicate (the reference's structural check,
+            // schedule.py:134-156; ranges are checked by the stream)
+            uint32_t *bt = reinterpret_cast<uint32_t *>(cbase + CL.bits);
             while (rs.i < rs.L) {
                 const int op = rs.o[0];
                 const int c = op_customer(op);
+                {
+                    const uint32_t bit = 1u << (op & 31);
+                    dup |= (atomicOr(&bt[op >> 5], bit) & bit) != 0;
+                }
                 const TT tn = t + (TT)rs.leg0();
                 if (NARROW) ovf |= tn < t;  // uint32 wrap -> 64-bit fix-up pass
                 t = tn;
@@ -529,7 +537,7 @@ makespan_kernel(DevInstance I, const OpT *__restrict__ ops, int64_t stride,
                 for (int j = rs.i; j < rs.L; ++j) cap_step(rs.checked_at(j), k, s, lo, hi);
             bad_ops = rs.bad;
         }
-        mal = mal || ((__ballot_sync(VRP_FULL_MASK, live && bad_ops) & gmask) != 0);
+        mal = mal || ((__ballot_sync(VRP_FULL_MASK, live && (bad_ops || dup)) & gmask) != 0);
         const bool capfail = (__ballot_sync(VRP_FULL_MASK, live && lo > hi) & gmask) != 0;
         const bool gdead = (__ballot_sync(VRP_FULL_MASK, live && dead) & gmask) != 0;
         const bool govf = NARROW && (__ballot_sync(VRP_FULL_MASK, live && ovf) & gmask) != 0;
