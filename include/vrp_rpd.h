@@ -89,7 +89,9 @@ int vrp_makespan_batch(vrp_instance_t h, const void *ops, int32_t op_bytes, int6
 
 /* Full event records for evaluate (schedule.py:188-257): per op (same layout as
  * ops) the arrival and execution time, per vehicle the minimal initial load
- * (route_initial_load, schedule.py:159-185).  Validating (MODE_EVALUATE). */
+ * (route_initial_load, schedule.py:159-185).  Validating (MODE_EVALUATE).
+ * Records are defined for candidates with status VRP_OK (every op executed),
+ * as the reference's Schedule exists only for those. */
 int vrp_evaluate_records(vrp_instance_t h, const int32_t *ops, int64_t op_stride,
                          const int32_t *lens, int64_t N, double *z, int32_t *status,
                          double *returns, double *arrival, double *time, int32_t *q0,

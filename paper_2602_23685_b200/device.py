@@ -148,9 +148,11 @@ def evaluate_records(instance, ops, lens, stream=None):
     res = {"z": torch.empty(Nc, dtype=torch.float64, device=dev),
            "status": torch.empty(Nc, dtype=torch.int32, device=dev),
            "returns": torch.empty((Nc, di.m), dtype=torch.float64, device=dev),
-           "arrival": torch.zeros(ops.shape, dtype=torch.float64, device=dev),
-           "time": torch.zeros(ops.shape, dtype=torch.float64, device=dev),
-           "q0": torch.zeros((Nc, di.m), dtype=torch.int32, device=dev)}
+           # defined for status-OK candidates (every op executed), like the
+           # reference's Schedule, which only exists for those
+           "arrival": torch.empty(ops.shape, dtype=torch.float64, device=dev),
+           "time": torch.empty(ops.shape, dtype=torch.float64, device=dev),
+           "q0": torch.empty((Nc, di.m), dtype=torch.int32, device=dev)}
     N.check(N.lib().vrp_evaluate_records(di.handle, N.ptr(ops), row_stride(ops), N.ptr(lens), Nc,
                                          N.ptr(res["z"]), N.ptr(res["status"]),
                                          N.ptr(res["returns"]), N.ptr(res["arrival"]),
