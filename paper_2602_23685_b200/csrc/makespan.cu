@@ -42,10 +42,10 @@ constexpr uint32_t NOT_READY32 = 0xFFFFFFFFu;
 constexpr int OPS_AHEAD = 8;   // op codes in registers (positions i .. i+7)
 constexpr int LEGS_AHEAD = 4;  // gathered legs in registers (positions i .. i+3)
 #ifndef K2_LEGS_AHEAD
-#define K2_LEGS_AHEAD 8  // two-pass (K2) pipeline depths: shared memory caps K2 at 8 warps/SM (4 / 8: 1.78 s, 8 / 12: 1.70 s LS cross pass at n = 999)
+#define K2_LEGS_AHEAD 12  // two-pass (K2) pipeline depths: shared memory caps K2 at 8 warps/SM (LS cross pass at n = 999, legs / ops: 4 / 8 1.78 s, 8 / 12 1.70 s; after the pass-1 duplicate check 8 / 12 1.53 s, 12 / 16 1.48 s)
 #endif
 #ifndef K2_OPS_AHEAD
-#define K2_OPS_AHEAD 12
+#define K2_OPS_AHEAD 16
 #endif
 #ifndef VRP_K1_RA
 #define VRP_K1_RA 0  // run-ahead ops per lockstep round (exact mode, slot table); measured slower, see DESIGN.md
